@@ -1,0 +1,428 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the Fastron FK hot path on B200.
+
+Step = one pass of the proxy-collision-check path over one batch: batched FK of Q
+query configurations (fastron_fk, K1) + FK-kernel scores and labels against the packed
+support set (fastron_score_packed, K2). Workload (BASELINE.json north_star, DESIGN.md
+R14): cfg2's 7-DOF arm, M = 8 control points, |S| = 20,000 supports (alpha ~ N(0,1)),
+Q = 1,000,000 uniform queries per GPU, gamma = 5, Gaussian term. Metric: collision
+checks/s (and kernel evaluations/s = checks/s x |S|); roofline = MUFU (SFU) throughput.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--rows]
+
+Multi-GPU (torchrun, one rank per GPU): every rank scores its own 1M-query batch against
+the replicated model — queries are independent units, so there is no data-path
+collective ("scaling": "weak"); timing is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "7-DOF FK-kernel proxy collision checks/sec (1M queries x 20k supports, M=8)"
+UNIT = "checks/s"
+MUFU_PER_CLK_PER_SM = 16  # B200 SFU: 16 ex2/rcp per clock per SM (tools/pipe_peaks.cu measured 15.8)
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            if self.thread:
+                self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_baseline(wl, target_s=12.0):
+    """The oracle as it stands, on this host's cores, on a bounded sample of the workload:
+    the first Qs queries of the batch against all supports (FK + fp64 score)."""
+    import oracle
+    spos = oracle.fk(wl.robot, wl.supports)
+
+    def run(nq):
+        t = time.perf_counter()
+        f, _ = oracle.score(wl.kind, wl.gamma, oracle.fk(wl.robot, wl.queries[:nq]), spos, wl.alpha)
+        return time.perf_counter() - t
+
+    t64 = run(64)
+    nq = int(min(len(wl.queries), max(64, 64 * target_s / max(t64, 1e-6))))
+    dt = run(nq)
+    return {"value": nq / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"first {nq} of the {len(wl.queries)} headline queries x all {len(wl.supports)} supports "
+                      f"(fp64 FK + score, OpenMP), {dt:.1f} s",
+            "kernel_evals_per_s": nq * len(wl.supports) / dt}
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import oracle
+    wl = W.score_workload("headline", kind=args.kind)
+    spos = oracle.fk(wl.robot, wl.supports)
+    # each step: a bounded sample of the batch (a different slice per step)
+    t0 = time.perf_counter()
+    oracle.score(wl.kind, wl.gamma, oracle.fk(wl.robot, wl.queries[:64]), spos, wl.alpha)
+    per_q = (time.perf_counter() - t0) / 64
+    nq = int(max(64, min(20000, 2.0 / max(per_q, 1e-9))))  # ~2 s of CPU per step
+    for s in range(args.warmup):
+        oracle.score(wl.kind, wl.gamma, oracle.fk(wl.robot, wl.queries[:64]), spos, wl.alpha)
+    t = time.perf_counter()
+    for s in range(args.steps):
+        sl = slice(s * nq, (s + 1) * nq)
+        oracle.score(wl.kind, wl.gamma, oracle.fk(wl.robot, wl.queries[sl]), spos, wl.alpha)
+    dt = (time.perf_counter() - t) / args.steps
+    value = nq / dt
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "headline", "n_supports": len(wl.supports), "queries_per_step": nq,
+                       "n_cp": wl.robot.n_cp, "dof": wl.robot.dof, "gamma": wl.gamma,
+                       "kernel": "gaussian" if wl.kind == 0 else "rq"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": f"{nq} queries x {len(wl.supports)} supports per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _time_rows(fb, torch, kind):
+    """Secondary §8(a) rows, each timed on its own (not part of the headline step)."""
+    rows = {}
+    st = torch.cuda.current_stream()
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            fn()
+        e1.record(st)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    # cfg1: 3-DOF, 10k queries x 1k supports, M=4 (launch-latency scale)
+    wl = W.score_workload("cfg1")
+    spos = fb.fastron_fk(wl.robot, torch.from_numpy(wl.supports).cuda())
+    model = fb.fastron_model_pack(spos, torch.from_numpy(wl.alpha).cuda(), kind, wl.gamma)
+    q = torch.from_numpy(wl.queries).cuda()
+    qpos = torch.empty((wl.robot.n_cp, len(wl.queries), 4), device="cuda")
+    sc = torch.empty(len(wl.queries), device="cuda")
+    lb = torch.empty(len(wl.queries), dtype=torch.int8, device="cuda")
+    wsb = torch.empty(max(256, fb.load_library().fastron_score_packed_workspace_bytes(len(wl.queries), len(wl.supports),
+                                                                                    wl.robot.n_cp)),
+                      dtype=torch.uint8, device="cuda")
+
+    def step1():
+        fb.fastron_fk(wl.robot, q, pos=qpos)
+        fb.fastron_score_packed(qpos, model, sc, lb, workspace=wsb)
+
+    ms = timed(step1, 50)
+    rows["cfg1_score"] = {"ms": ms, "checks_per_s": len(wl.queries) / ms * 1e3,
+                          "kernel_evals_per_s": len(wl.queries) * len(wl.supports) / ms * 1e3}
+    # cfg2: 1M x 2k, M=8
+    wl = W.score_workload("cfg2")
+    spos = fb.fastron_fk(wl.robot, torch.from_numpy(wl.supports).cuda())
+    model = fb.fastron_model_pack(spos, torch.from_numpy(wl.alpha).cuda(), kind, wl.gamma)
+    q = torch.from_numpy(wl.queries).cuda()
+    qpos = torch.empty((8, len(wl.queries), 4), device="cuda")
+    sc = torch.empty(len(wl.queries), device="cuda")
+    lb = torch.empty(len(wl.queries), dtype=torch.int8, device="cuda")
+
+    def step2():
+        fb.fastron_fk(wl.robot, q, pos=qpos)
+        fb.fastron_score_packed(qpos, model, sc, lb)
+
+    ms = timed(step2, 10)
+    rows["cfg2_score"] = {"ms": ms, "checks_per_s": len(wl.queries) / ms * 1e3,
+                          "kernel_evals_per_s": len(wl.queries) * len(wl.supports) / ms * 1e3}
+    # cfg3: Gram 5000^2 + Algorithm 1 (labels from the product FK + the workload labeller)
+    tw = W.train_workload()
+    X = torch.from_numpy(tw.X).cuda()
+    pos = fb.fastron_fk(tw.robot, X)
+    P = np.transpose(pos.cpu().numpy()[:, :, :3], (1, 0, 2)).astype(np.float64)
+    y = torch.from_numpy(W.capsule_aabb_labels(W.chain_points(P), tw.cubes, tw.radius)).cuda()
+    K = torch.empty((len(tw.X), len(tw.X)), device="cuda")
+    gws = torch.empty(fb.load_library().fastron_gram_workspace_bytes(len(tw.X), 8), dtype=torch.uint8, device="cuda")
+    ms = timed(lambda: fb.fastron_gram(pos, tw.kind, tw.gamma, K=K, workspace=gws), 10)
+    n = len(tw.X)
+    rows["cfg3_gram"] = {"ms": ms, "unique_pairs": n * (n + 1) // 2,
+                         "mufu_tops": n * n * 8 / 2 / ms * 1e-9, "write_GBps": n * n * 4 / ms * 1e-6}
+    out = {}
+
+    def train():
+        out.update(fb.fastron_train(K, y, tw.beta, tw.iter_max))
+
+    ms = timed(train, 3)
+    res = fb.train_result(out["result"])
+    rows["cfg3_train"] = {"ms": ms, **res, "us_per_iteration": ms * 1e3 / max(res["iterations"], 1),
+                          "positive_fraction": float((y > 0).float().mean().item())}
+    # cfg4: 10k edges x 64 points, 3k supports, early exit
+    ew = W.edge_workload()
+    spos = fb.fastron_fk(ew.robot, torch.from_numpy(ew.supports).cuda())
+    qa, qb = torch.from_numpy(ew.qa).cuda(), torch.from_numpy(ew.qb).cuda()
+    al = torch.from_numpy(ew.alpha).cuda()
+    res = {}
+
+    def edges():
+        res["hit"], res["idx"] = fb.fastron_edge_check(ew.robot, qa, qb, ew.n_interp, spos, al, kind, ew.gamma)
+
+    ms = timed(edges, 5)
+    idx = res["idx"].cpu().numpy()
+    hit = res["hit"].cpu().numpy()
+    order = [2 * o for o in range(32)] + [2 * o + 1 for o in range(32)]
+    pos_of = {k: o for o, k in enumerate(order)}
+    rounds = np.array([1 if (h and pos_of[int(k)] < 32) else 2 for h, k in zip(hit, idx)])
+    evaluated = int(np.sum(rounds * 32))
+    rows["cfg4_edges"] = {"ms": ms, "edges_per_s": len(ew.qa) / ms * 1e3, "in_collision_fraction": float(hit.mean()),
+                          "configs_evaluated": evaluated,
+                          "evaluated_kernel_evals_per_s": evaluated * len(ew.supports) / ms * 1e3}
+    return rows
+
+
+def run_ours(args):
+    import torch
+    import paper_1910_06451_b200 as fb
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    fb.load_library()
+    wl = W.score_workload("headline", kind=args.kind)
+    Q, S, M = len(wl.queries), len(wl.supports), wl.robot.n_cp
+    queries = wl.queries if rank == 0 else W.uniform_configs(np.random.default_rng(1000 + rank), Q, wl.robot.dof)
+    robot = fb.make_robot_struct(wl.robot)
+    st = torch.cuda.current_stream()
+
+    # model (support set): FK + pack once per model update
+    spos = fb.fastron_fk(robot, torch.from_numpy(wl.supports).cuda())
+    model = fb.fastron_model_pack(spos, torch.from_numpy(wl.alpha).cuda(), wl.kind, wl.gamma)
+    q = torch.from_numpy(queries).cuda()
+    qpos = torch.empty((M, Q, 4), device="cuda")
+    score = torch.empty(Q, device="cuda")
+    label = torch.empty(Q, dtype=torch.int8, device="cuda")
+    wsb = torch.empty(max(256, fb.load_library().fastron_score_packed_workspace_bytes(Q, S, M)), dtype=torch.uint8,
+                      device="cuda")
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+
+    def step(e=None):
+        if e:
+            e[0].record(st)
+        fb.fastron_fk(robot, q, pos=qpos)
+        if e:
+            e[1].record(st)
+        fb.fastron_score_packed(qpos, model, score, label, workspace=wsb)
+        if e:
+            e[2].record(st)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    launches0 = fb.launch_count()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(st)
+        for s in range(args.steps):
+            step(ev[s])
+        t1.record(st)
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+    launches = fb.launch_count() - launches0
+    ms_total = t0.elapsed_time(t1)
+    fk_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
+    sc_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
+    ms_step = ms_total / args.steps
+    if ws > 1:
+        t = torch.tensor([ms_step], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_step = float(t.item())
+    value = ws * Q / (ms_step * 1e-3)
+    clocks = clk.summary()
+
+    # ---- end to end through the public API with host buffers (pinned), rank-local ----
+    qh = torch.from_numpy(queries).pin_memory()
+    sh = torch.empty(Q, dtype=torch.float32).pin_memory()
+    lh = torch.empty(Q, dtype=torch.int8).pin_memory()
+    qws = torch.empty(fb.load_library().fastron_query_workspace_bytes(Q, S, M, wl.robot.dof), dtype=torch.uint8,
+                      device="cuda")
+
+    def e2e_step():
+        fb.fastron_query(robot, qh, spos, model_alpha, wl.kind, wl.gamma, score=sh, label=lh, workspace=qws)
+
+    model_alpha = torch.from_numpy(wl.alpha).cuda()
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(st)
+    e1.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    if ws > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    assert np.array_equal(sh.numpy(), score.cpu().numpy()), "fastron_query disagrees with fk + score_packed"
+
+    # ---- roofline of the dominant kernel (the score launch) ----
+    peaks = _peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    peak = sms * MUFU_PER_CLK_PER_SM * sm_max * 1e6  # MUFU ops/s at the max SM clock
+    achieved = Q * S * M / (sc_ms * 1e-3)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "score_traffic.json")) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    roof = {"bound": "alu", "pipe": "MUFU (SFU) ex2" if wl.kind == 0 else "MUFU (SFU) rcp",
+            "achieved": achieved * 1e-12, "peak": peak * 1e-12, "unit": "Tops/s", "frac": achieved / peak,
+            "traffic": traffic, "kernel": "fastron_score_packed (score_kernel<8,kind,pos> + finalize)",
+            "peak_source": f"{sms} SMs x {MUFU_PER_CLK_PER_SM} MUFU/clk x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+            "frac_at_run_clock": (achieved / (sms * MUFU_PER_CLK_PER_SM * clocks["sm_mhz"] * 1e6)
+                                  if clocks.get("sm_mhz") else None),
+            "kernel_ms": sc_ms, "fk_ms": fk_ms,
+            "fk_hbm_GBps": Q * (wl.robot.dof * 4 + M * 16) / (fk_ms * 1e-3) * 1e-9,
+            "fk_hbm_frac": Q * (wl.robot.dof * 4 + M * 16) / (fk_ms * 1e-3) * 1e-9 / float(peaks.get("hbm_gbs", 6554.6))}
+
+    rows = None
+    if args.rows and rank == 0:
+        rows = _time_rows(fb, torch, args.kind)
+
+    base = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        base = cpu_baseline(W.score_workload("headline", kind=args.kind))
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32 (fp64 FK and accumulation)", "data": "synthetic",
+                "config": {"workload": "headline", "model": "cfg2 7-DOF arm, M=8", "global_batch": ws * Q,
+                           "queries_per_gpu": Q, "n_supports": S, "n_cp": M, "dof": wl.robot.dof,
+                           "gamma": wl.gamma, "kernel": "gaussian" if wl.kind == 0 else "rq",
+                           "parallelism": f"dp{ws} (query shards, replicated model)",
+                           "l2": "inputs larger than L2 (28 MB queries + 128 MB positions per step > 126 MB)"},
+                "kernel_evals_per_s": value * S,
+                "roofline": roof,
+                "cpu_baseline": base,
+                "e2e": {"value": ws * Q / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": Q * wl.robot.dof * 4,
+                        "d2h_bytes_per_step": Q * 5, "ms_per_step": e2e_ms,
+                        "api": "fastron_query with pinned host q/score/label"},
+                "gpu_launches": launches,
+                "clocks": clocks}
+        if rows is not None:
+            line["rows"] = rows
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--kind", type=int, default=0, help="0 = Gaussian (north star), 1 = RQ (PAPER.md Eq. 3)")
+    ap.add_argument("--rows", action="store_true", help="also time cfg1/cfg2/cfg3/cfg4 rows")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,223 @@
+/*
+ * fastron.h — C ABI of the B200-native Fastron FK hot path (arXiv 1910.06451,
+ * "Forward Kinematics Kernel for Improved Proxy Collision Checking").
+ *
+ * Library: paper_1910_06451_b200/libfastron_b200.so (hand-written sm_100a CUDA).
+ * Citations: PAPER.md:<line> (§, Eq./Alg.) of /root/reference/PAPER.md; readings
+ * R<n> are listed in DESIGN.md §3.
+ *
+ * Conventions for every call
+ * --------------------------
+ *  - Pointers are DEVICE pointers unless the argument says "host" (or "host or
+ *    device" for fastron_query). The caller owns every buffer; the library never
+ *    allocates or frees caller memory and keeps no state besides a per-device cache
+ *    of cudaDeviceProp/occupancy. Scratch memory is passed in through `workspace`.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Calls enqueue work on it and return without synchronising (except where noted);
+ *    asynchronous device faults surface at the caller's next synchronisation.
+ *  - Host-checkable argument errors return FASTRON_ERR_INVALID_ARG before any launch:
+ *    null pointers with a non-zero size, negative sizes, leading dimensions smaller
+ *    than the row length, gamma <= 0 or non-finite, unknown kernel kind, dof outside
+ *    [1,16], n_cp outside [1,32], cp_frame outside [0,dof], non-finite robot data,
+ *    beta < 1, n_interp < 1. A short workspace returns FASTRON_ERR_WORKSPACE. A
+ *    CUDA launch/runtime failure returns FASTRON_ERR_CUDA. fastron_last_error()
+ *    returns a thread-local message for the last non-OK status of the calling thread.
+ *  - Device array CONTENTS (NaN joint values, labels outside {-1,+1}) are not
+ *    checked on the hot path.
+ *  - There is no CPU fallback: every computation runs in this library's kernels.
+ *
+ * Data layouts
+ * ------------
+ *  Configurations q: row-major float [n][ldq], columns 0..dof-1 used.
+ *  Control-point positions: SoA float4 [n_cp][ldpos] = (x, y, z, 0) in metres,
+ *    i.e. element (m, k) at pos + 4*(m*ldpos + k) (Eq. 2).
+ *  Gram matrix: row-major float [n][ldk].
+ */
+#ifndef FASTRON_H_
+#define FASTRON_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FASTRON_MAX_DOF 16
+#define FASTRON_MAX_CP 32
+
+typedef enum {
+  FASTRON_OK = 0,
+  FASTRON_ERR_INVALID_ARG = 1,
+  FASTRON_ERR_CUDA = 2,
+  FASTRON_ERR_WORKSPACE = 3,
+  FASTRON_ERR_UNSUPPORTED = 4
+} fastron_status;
+
+/* Shape of the per-control-point RBF term (R1/R2). Both are combined by
+ * the 1/M mean of Eq. 4, so k(x, x) = 1 for both. */
+typedef enum {
+  FASTRON_RBF_GAUSSIAN = 0, /* exp(-gamma d^2): BASELINE.json north_star term (headline)  */
+  FASTRON_RBF_RQ = 1        /* (1 + gamma/2 d^2)^-2: Eq. 3               */
+} fastron_rbf;
+
+typedef struct {
+  int32_t kind; /* fastron_rbf */
+  float gamma;  /* > 0 and finite */
+} fastron_kernel;
+
+/* Serial manipulator in the standard D-H convention with its
+ * control points. Host struct; copied by value into kernel parameters. */
+typedef struct {
+  int32_t dof;                  /* D in [1, 16]; all joints revolute (R6)             */
+  int32_t n_cp;                 /* M in [1, 32]                                        */
+  float dh[FASTRON_MAX_DOF][4]; /* per joint: theta_offset, d, a, alpha (Eq. 1);
+                                   theta_i = q_i + theta_offset_i                     */
+  float base[3][4];             /* wA_0 as a row-major 3x4 affine       */
+  int32_t cp_frame[FASTRON_MAX_CP];     /* j_m in [0, D]: 0 = base frame, i = frame
+                                           after joint i (Eq. 2)                       */
+  float cp_offset[FASTRON_MAX_CP][3];   /* translation of the static T_m in frame j_m
+                                           (T_m = I <=> 0)               */
+} fastron_robot;
+
+typedef struct {
+  int64_t iterations; /* add/adjust + remove steps taken (R10)                      */
+  int64_t n_add;      /* add/adjust steps (Eq. 6-8)                                  */
+  int64_t n_remove;   /* redundant-support removals (Alg. 1 lines PAPER.md:235-239) */
+  int32_t converged;  /* 1 iff min_i y_i F_i > 0 at exit (Claim 2)     */
+  int32_t n_support;  /* |S| = count(alpha != 0) after removeNonsupportPoints         */
+} fastron_train_result;
+
+/*
+ * fastron_fk — batched forward kinematics, Eq. 1-2.
+ * For k < n: theta_i = q[k*ldq + i] + theta_offset_i, wA_i = wA_0 0A_1 ... (i-1)A_i,
+ * pos(m, k) = pos(wA_{j_m} T_m). Arithmetic is fp64 inside (sincos, chain), rounded
+ * once to fp32 on store. One thread per configuration.
+ *   robot: host. q: device float [n][ldq], ldq >= dof. pos: device float4 [n_cp][ldpos],
+ *   ldpos >= n, 16-byte aligned. n == 0 is a no-op.
+ */
+fastron_status fastron_fk(const fastron_robot* robot, const float* q, int64_t n, int64_t ldq, float* pos,
+                          int64_t ldpos, void* stream);
+
+/*
+ * fastron_score — Fastron model evaluation f(x) = sum_i K_FK(S_i, x) alpha_i and its
+ * sign, K_FK of Eq. 4 with the term of k.kind.
+ *   qpos: device float4 [n_cp][ldq] query control points (from fastron_fk), ldq >= nq.
+ *   spos: device float4 [n_cp][lds] support control points, lds >= ns. alpha: device float [ns].
+ *   score: device float [nq] (nullable): f rounded to fp32 (accumulated in fp64).
+ *   label: device int8 [nq] (nullable): +1 iff f > 0 else -1 (R8).
+ *   workspace: device scratch of >= fastron_score_workspace_bytes(nq, ns, n_cp) bytes,
+ *   256-byte aligned; contents are overwritten.
+ * ns == 0 gives f = 0, label -1. nq == 0 is a no-op.
+ * Results are deterministic (fixed-order reductions) for a given device.
+ */
+size_t fastron_score_workspace_bytes(int64_t nq, int64_t ns, int32_t n_cp);
+fastron_status fastron_score(const float* qpos, int64_t nq, int64_t ldq, const float* spos, const float* alpha,
+                             int64_t ns, int64_t lds, int32_t n_cp, fastron_kernel k, float* score, int8_t* label,
+                             void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * fastron_model_pack / fastron_score_packed — the same evaluation as fastron_score, split
+ * so that a model (support positions + alpha, "support set") is packed once
+ * per model update and then scored against many query batches.
+ *   fastron_model_pack: spos/alpha as fastron_score; packed: device buffer of
+ *   fastron_model_bytes(ns, n_cp) bytes, 256-byte aligned, holding the supports
+ *   pre-scaled for kernel k (its contents are only meaningful to fastron_score_packed
+ *   with the same ns, n_cp and k).
+ *   fastron_score_packed: qpos/score/label as fastron_score; workspace >=
+ *   fastron_score_packed_workspace_bytes(nq, ns, n_cp) (may be 0 bytes).
+ */
+size_t fastron_model_bytes(int64_t ns, int32_t n_cp);
+fastron_status fastron_model_pack(const float* spos, const float* alpha, int64_t ns, int64_t lds, int32_t n_cp,
+                                  fastron_kernel k, void* packed, size_t packed_bytes, void* stream);
+size_t fastron_score_packed_workspace_bytes(int64_t nq, int64_t ns, int32_t n_cp);
+fastron_status fastron_score_packed(const float* qpos, int64_t nq, int64_t ldq, const void* packed, int64_t ns,
+                                    int32_t n_cp, fastron_kernel k, float* score, int8_t* label, void* workspace,
+                                    size_t workspace_bytes, void* stream);
+
+/*
+ * fastron_gram — FK-kernel Gram matrix K_ij = K_FK(X_i, X_j),
+ * written in full (both triangles; computed once per unordered pair and mirrored,
+ * so K is exactly symmetric, and K_ii = 1 exactly for n_cp a power of two).
+ * Values are bit-identical to fastron_score with alpha = e_i.
+ *   pos: device float4 [n_cp][ldp], ldp >= n. K: device float [n][ldk], ldk >= n.
+ *   workspace: >= fastron_gram_workspace_bytes(n, n_cp).
+ */
+size_t fastron_gram_workspace_bytes(int64_t n, int32_t n_cp);
+fastron_status fastron_gram(const float* pos, int64_t n, int64_t ldp, int32_t n_cp, fastron_kernel k, float* K,
+                            int64_t ldk, void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * fastron_train — Algorithm 1, "Fastron Model Update Algorithm" (PAPER.md:206-252,
+ * Eq. 6-9), run entirely on the device in one persistent cluster kernel.
+ *   K: device float [n][ldk] Gram (from fastron_gram; promoted to fp64 on read).
+ *   y: device int8 [n], +1 = C_obs, -1 = C_free.
+ *   beta >= 1: conditional bias, b_i = beta^(0.5 (y_i + 1)).
+ *   iter_max >= 0, s_max >= 0.
+ *   alpha_inout, F_inout: device double [n]; on entry the previous model
+ *     (loadPreviousModel; zeros = cold start; F must equal K alpha),
+ *     on exit the updated alpha and F.
+ *   support_idx: device int32 [n] (nullable): ascending indices with alpha != 0
+ *     (removeNonsupportPoints); result->n_support entries are valid.
+ *   trace: device int32 [iter_max] (nullable): i for an add/adjust of i, -(i+1) for a
+ *     removal of i, one entry per iteration.
+ *   result: device fastron_train_result.
+ * Ties in argmin/argmax go to the lowest index (R9); an iteration is one add/adjust
+ * or remove (R10); non-convergence is reported in result->converged, not as an error.
+ * All alpha/F arithmetic is fp64 with separately rounded multiply and add, so the
+ * trace is bit-identical to the oracle's on the same K (R13).
+ * n <= fastron_train_max_n() (state is held on chip); larger n returns ERR_UNSUPPORTED.
+ */
+int64_t fastron_train_max_n(void);
+fastron_status fastron_train(const float* K, int64_t n, int64_t ldk, const int8_t* y, double beta, int64_t iter_max,
+                             int64_t s_max, double* alpha_inout, double* F_inout, int32_t* support_idx,
+                             int32_t* trace, fastron_train_result* result, void* stream);
+
+/*
+ * fastron_edge_check — discrete motion-planning edge check (BASELINE.json cfg4,
+ * SPEC.md:379-387, R11): for edge e and k = 0..n_interp-1,
+ * q_k = qa + t_k (qb - qa) with t_k = k / (n_interp - 1) in fp32 (t = 0 if n_interp = 1),
+ * each q_k goes through FK (Eq. 1-2) and the Fastron score;
+ * in_collision[e] = 1 iff some f(q_k) > 0. Points are visited in rounds of 32 in the
+ * order k = 0, 2, 4, ..., then 1, 3, 5, ...; an edge stops after the first round that
+ * contains a hit (warp vote).
+ *   robot: host. qa, qb: device float [n_edges][ldq]. spos/alpha as fastron_score.
+ *   in_collision: device uint8 [n_edges]. hit_index: device int32 [n_edges] (nullable):
+ *   the lowest k with f(q_k) > 0 inside the first round that had a hit, else -1.
+ *   workspace: >= fastron_edge_workspace_bytes(n_edges, ns, robot->n_cp).
+ */
+size_t fastron_edge_workspace_bytes(int64_t n_edges, int64_t ns, int32_t n_cp);
+fastron_status fastron_edge_check(const fastron_robot* robot, const float* qa, const float* qb, int64_t n_edges,
+                                  int64_t ldq, int32_t n_interp, const float* spos, const float* alpha, int64_t ns,
+                                  int64_t lds, fastron_kernel k, uint8_t* in_collision, int32_t* hit_index,
+                                  void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * fastron_query — the configuration-level proxy collision check, fastron_fk followed
+ * by fastron_score on the same stream ("query").
+ *   q: float [nq][ldq], HOST (pageable or pinned) or DEVICE. score (nullable) and
+ *   label (nullable): HOST or DEVICE. spos/alpha: device, as fastron_score.
+ *   When q / score / label are host memory the call streams them in chunks through the
+ *   workspace (H2D of chunk c+1 overlaps compute of chunk c) and returns after the
+ *   results are in host memory (it synchronises `stream`). With device pointers it is
+ *   asynchronous like the other calls.
+ *   workspace: >= fastron_query_workspace_bytes(nq, ns, robot->n_cp, robot->dof).
+ */
+size_t fastron_query_workspace_bytes(int64_t nq, int64_t ns, int32_t n_cp, int32_t dof);
+fastron_status fastron_query(const fastron_robot* robot, const float* q, int64_t nq, int64_t ldq, const float* spos,
+                             const float* alpha, int64_t ns, int64_t lds, fastron_kernel k, float* score,
+                             int8_t* label, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Thread-local message for the last non-OK status returned on this thread. */
+const char* fastron_last_error(void);
+
+/* Library version string and the number of kernel launches issued by this process
+ * (a counter for the bench's gpu_launches claim). */
+const char* fastron_version(void);
+int64_t fastron_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FASTRON_H_ */

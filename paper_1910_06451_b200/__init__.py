@@ -1,0 +1,338 @@
+"""Thin Python binding of libfastron_b200.so (include/fastron.h).
+
+Argument marshalling only: every step of the hot path runs in the library's sm_100a
+kernels. PyTorch provides device memory and streams. The functions keep the C names
+(fastron_fk, fastron_score, fastron_gram, fastron_train, fastron_edge_check,
+fastron_query) and take torch tensors; outputs are allocated when not given.
+
+There is no CPU fallback: importing this package without the built library, or
+calling it without a CUDA device, raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfastron_b200.so")
+
+FASTRON_OK, FASTRON_ERR_INVALID_ARG, FASTRON_ERR_CUDA, FASTRON_ERR_WORKSPACE, FASTRON_ERR_UNSUPPORTED = range(5)
+GAUSSIAN, RQ = 0, 1
+MAX_DOF, MAX_CP = 16, 32
+
+# Symbols declared in include/fastron.h (checked by tests/test_abi_cpu.py).
+EXPORTED = [
+    "fastron_fk", "fastron_score_workspace_bytes", "fastron_score", "fastron_gram_workspace_bytes", "fastron_gram",
+    "fastron_train_max_n", "fastron_train", "fastron_edge_workspace_bytes", "fastron_edge_check",
+    "fastron_query_workspace_bytes", "fastron_query", "fastron_last_error", "fastron_version",
+    "fastron_launch_count", "fastron_model_bytes", "fastron_model_pack", "fastron_score_packed_workspace_bytes",
+    "fastron_score_packed",
+]
+
+
+class FastronError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"fastron status {status}: {message}")
+        self.status = status
+
+
+class fastron_kernel(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("gamma", ctypes.c_float)]
+
+
+class fastron_robot(ctypes.Structure):
+    _fields_ = [
+        ("dof", ctypes.c_int32),
+        ("n_cp", ctypes.c_int32),
+        ("dh", (ctypes.c_float * 4) * MAX_DOF),
+        ("base", (ctypes.c_float * 4) * 3),
+        ("cp_frame", ctypes.c_int32 * MAX_CP),
+        ("cp_offset", (ctypes.c_float * 3) * MAX_CP),
+    ]
+
+
+class fastron_train_result(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int64), ("n_add", ctypes.c_int64), ("n_remove", ctypes.c_int64),
+                ("converged", ctypes.c_int32), ("n_support", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load the in-tree library (build it first with paper_1910_06451_b200._build)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with `python -m paper_1910_06451_b200._build` "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(path)
+    vp, i64, i32, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
+    st = ctypes.c_int
+    rp = ctypes.POINTER(fastron_robot)
+    L.fastron_fk.argtypes = [rp, vp, i64, i64, vp, i64, vp]
+    L.fastron_score_workspace_bytes.argtypes = [i64, i64, i32]
+    L.fastron_score_workspace_bytes.restype = sz
+    L.fastron_score.argtypes = [vp, i64, i64, vp, vp, i64, i64, i32, fastron_kernel, vp, vp, vp, sz, vp]
+    L.fastron_model_bytes.argtypes = [i64, i32]
+    L.fastron_model_bytes.restype = sz
+    L.fastron_model_pack.argtypes = [vp, vp, i64, i64, i32, fastron_kernel, vp, sz, vp]
+    L.fastron_score_packed_workspace_bytes.argtypes = [i64, i64, i32]
+    L.fastron_score_packed_workspace_bytes.restype = sz
+    L.fastron_score_packed.argtypes = [vp, i64, i64, vp, i64, i32, fastron_kernel, vp, vp, vp, sz, vp]
+    L.fastron_gram_workspace_bytes.argtypes = [i64, i32]
+    L.fastron_gram_workspace_bytes.restype = sz
+    L.fastron_gram.argtypes = [vp, i64, i64, i32, fastron_kernel, vp, i64, vp, sz, vp]
+    L.fastron_train_max_n.argtypes = []
+    L.fastron_train_max_n.restype = i64
+    L.fastron_train.argtypes = [vp, i64, i64, vp, ctypes.c_double, i64, i64, vp, vp, vp, vp, vp, vp]
+    L.fastron_edge_workspace_bytes.argtypes = [i64, i64, i32]
+    L.fastron_edge_workspace_bytes.restype = sz
+    L.fastron_edge_check.argtypes = [rp, vp, vp, i64, i64, i32, vp, vp, i64, i64, fastron_kernel, vp, vp, vp, sz, vp]
+    L.fastron_query_workspace_bytes.argtypes = [i64, i64, i32, i32]
+    L.fastron_query_workspace_bytes.restype = sz
+    L.fastron_query.argtypes = [rp, vp, i64, i64, vp, vp, i64, i64, fastron_kernel, vp, vp, vp, sz, vp]
+    for f in ("fastron_fk", "fastron_score", "fastron_gram", "fastron_train", "fastron_edge_check", "fastron_query",
+              "fastron_model_pack", "fastron_score_packed"):
+        getattr(L, f).restype = st
+    L.fastron_last_error.argtypes = []
+    L.fastron_last_error.restype = ctypes.c_char_p
+    L.fastron_version.argtypes = []
+    L.fastron_version.restype = ctypes.c_char_p
+    L.fastron_launch_count.argtypes = []
+    L.fastron_launch_count.restype = i64
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != FASTRON_OK:
+        raise FastronError(status, _lib.fastron_last_error().decode())
+
+
+def make_robot_struct(robot) -> fastron_robot:
+    """Marshal any object with dof, dh (D,4), base (3,4), cp_frame (M,), cp_offset (M,3)."""
+    r = fastron_robot()
+    dh = np.asarray(robot.dh, dtype=np.float32)
+    D = dh.shape[0]
+    cpf = np.asarray(robot.cp_frame, dtype=np.int32)
+    cpo = np.asarray(robot.cp_offset, dtype=np.float32).reshape(-1, 3)
+    M = cpf.shape[0]
+    if not (1 <= D <= MAX_DOF and 1 <= M <= MAX_CP):
+        raise ValueError("dof must be in [1,16] and n_cp in [1,32]")
+    r.dof, r.n_cp = D, M
+    for i in range(D):
+        for c in range(4):
+            r.dh[i][c] = float(dh[i, c])
+    base = np.asarray(robot.base, dtype=np.float32)
+    for i in range(3):
+        for c in range(4):
+            r.base[i][c] = float(base[i, c])
+    for m in range(M):
+        r.cp_frame[m] = int(cpf[m])
+        for c in range(3):
+            r.cp_offset[m][c] = float(cpo[m, c])
+    return r
+
+
+def _stream(stream) -> Optional[int]:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _kernel(kind: int, gamma: float) -> fastron_kernel:
+    return fastron_kernel(int(kind), float(gamma))
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("device tensors required (no CPU fallback); use fastron_query for host buffers")
+
+
+def _workspace(nbytes: int, device):
+    import torch
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def fastron_fk(robot, q, pos=None, stream=None):
+    """q (n, >=D) float32 cuda -> pos (M, n, 4) float32 cuda (SoA float4, Eq. 1-2)."""
+    import torch
+    L = load_library()
+    _require_cuda(q, pos)
+    r = robot if isinstance(robot, fastron_robot) else make_robot_struct(robot)
+    n = q.shape[0]
+    if pos is None:
+        pos = torch.empty((r.n_cp, n, 4), dtype=torch.float32, device=q.device)
+    ldq = q.stride(0) if q.dim() == 2 else r.dof
+    _check(L.fastron_fk(ctypes.byref(r), _ptr(q), n, ldq, _ptr(pos), pos.stride(0) // 4, _stream(stream)))
+    return pos
+
+
+def fastron_score(qpos, spos, alpha, kind: int, gamma: float, score=None, label=None, want_score=True,
+                  want_label=True, workspace=None, stream=None):
+    """qpos (M, nq, 4), spos (M, ns, 4), alpha (ns,) -> (score float32 (nq,), label int8 (nq,))."""
+    import torch
+    L = load_library()
+    _require_cuda(qpos, spos, alpha)
+    M, nq = qpos.shape[0], qpos.shape[1]
+    ns = spos.shape[1]
+    if want_score and score is None:
+        score = torch.empty(nq, dtype=torch.float32, device=qpos.device)
+    if want_label and label is None:
+        label = torch.empty(nq, dtype=torch.int8, device=qpos.device)
+    need = L.fastron_score_workspace_bytes(nq, ns, M)
+    if workspace is None or workspace.numel() < need:
+        workspace = _workspace(need, qpos.device)
+    lds = spos.stride(0) // 4 if ns > 0 else 0
+    _check(L.fastron_score(_ptr(qpos), nq, qpos.stride(0) // 4, _ptr(spos) if ns else None,
+                           _ptr(alpha) if ns else None, ns, lds, M, _kernel(kind, gamma), _ptr(score), _ptr(label),
+                           _ptr(workspace), workspace.numel(), _stream(stream)))
+    return score, label
+
+
+class PackedModel:
+    """A support set packed once per model update (fastron_model_pack)."""
+
+    def __init__(self, buf, ns: int, n_cp: int, kind: int, gamma: float):
+        self.buf, self.ns, self.n_cp, self.kind, self.gamma = buf, ns, n_cp, kind, gamma
+
+
+def fastron_model_pack(spos, alpha, kind: int, gamma: float, stream=None) -> PackedModel:
+    L = load_library()
+    _require_cuda(spos, alpha)
+    M, ns = spos.shape[0], spos.shape[1]
+    buf = _workspace(L.fastron_model_bytes(ns, M), spos.device)
+    lds = spos.stride(0) // 4 if ns > 0 else 0
+    _check(L.fastron_model_pack(_ptr(spos) if ns else None, _ptr(alpha) if ns else None, ns, lds, M,
+                                _kernel(kind, gamma), _ptr(buf), buf.numel(), _stream(stream)))
+    return PackedModel(buf, ns, M, kind, gamma)
+
+
+def fastron_score_packed(qpos, model: PackedModel, score=None, label=None, want_score=True, want_label=True,
+                         workspace=None, stream=None):
+    import torch
+    L = load_library()
+    _require_cuda(qpos)
+    M, nq = qpos.shape[0], qpos.shape[1]
+    if M != model.n_cp:
+        raise ValueError("query and model control-point counts differ")
+    if want_score and score is None:
+        score = torch.empty(nq, dtype=torch.float32, device=qpos.device)
+    if want_label and label is None:
+        label = torch.empty(nq, dtype=torch.int8, device=qpos.device)
+    need = L.fastron_score_packed_workspace_bytes(nq, model.ns, M)
+    if workspace is None or workspace.numel() < need:
+        workspace = _workspace(need, qpos.device)
+    _check(L.fastron_score_packed(_ptr(qpos), nq, qpos.stride(0) // 4, _ptr(model.buf), model.ns, M,
+                                  _kernel(model.kind, model.gamma), _ptr(score), _ptr(label), _ptr(workspace),
+                                  workspace.numel(), _stream(stream)))
+    return score, label
+
+
+def fastron_gram(pos, kind: int, gamma: float, K=None, workspace=None, stream=None):
+    """pos (M, n, 4) -> K (n, n) float32."""
+    import torch
+    L = load_library()
+    _require_cuda(pos, K)
+    M, n = pos.shape[0], pos.shape[1]
+    if K is None:
+        K = torch.empty((n, n), dtype=torch.float32, device=pos.device)
+    need = L.fastron_gram_workspace_bytes(n, M)
+    if workspace is None or workspace.numel() < need:
+        workspace = _workspace(need, pos.device)
+    _check(L.fastron_gram(_ptr(pos), n, pos.stride(0) // 4, M, _kernel(kind, gamma), _ptr(K), K.stride(0),
+                          _ptr(workspace), workspace.numel(), _stream(stream)))
+    return K
+
+
+def fastron_train(K, y, beta: float = 1.0, iter_max: int = 20000, s_max: Optional[int] = None, alpha=None, F=None,
+                  support_idx=True, trace=True, result=None, stream=None):
+    """Algorithm 1 on device. Returns dict of device tensors (alpha, F, support_idx, trace)
+    and the result struct as a uint8 device tensor (decode with train_result())."""
+    import torch
+    L = load_library()
+    _require_cuda(K, y, alpha, F)
+    n = K.shape[0]
+    dev = K.device
+    s_max = n if s_max is None else int(s_max)
+    if alpha is None:
+        alpha = torch.zeros(n, dtype=torch.float64, device=dev)
+    if F is None:
+        F = torch.zeros(n, dtype=torch.float64, device=dev)
+    sup = torch.empty(max(n, 1), dtype=torch.int32, device=dev) if support_idx is True else support_idx
+    tr = torch.empty(max(iter_max, 1), dtype=torch.int32, device=dev) if trace is True else trace
+    res = torch.zeros(ctypes.sizeof(fastron_train_result), dtype=torch.uint8, device=dev) if result is None else result
+    _check(L.fastron_train(_ptr(K), n, K.stride(0) if n else 1, _ptr(y), float(beta), int(iter_max), s_max,
+                           _ptr(alpha), _ptr(F), _ptr(sup) if sup is not None and sup is not False else None,
+                           _ptr(tr) if tr is not None and tr is not False else None, _ptr(res), _stream(stream)))
+    return dict(alpha=alpha, F=F, support_idx=sup, trace=tr, result=res)
+
+
+def train_result(res_tensor) -> dict:
+    raw = bytes(res_tensor.cpu().numpy().tobytes())
+    r = fastron_train_result.from_buffer_copy(raw)
+    return dict(iterations=r.iterations, n_add=r.n_add, n_remove=r.n_remove, converged=bool(r.converged),
+                n_support=r.n_support)
+
+
+def fastron_edge_check(robot, qa, qb, n_interp: int, spos, alpha, kind: int, gamma: float, in_collision=None,
+                       hit_index=None, want_hit_index=True, workspace=None, stream=None):
+    import torch
+    L = load_library()
+    _require_cuda(qa, qb, spos, alpha)
+    r = robot if isinstance(robot, fastron_robot) else make_robot_struct(robot)
+    E = qa.shape[0]
+    ns = spos.shape[1]
+    if qa.shape != qb.shape or qa.stride(0) != qb.stride(0):
+        raise ValueError("qa and qb must have the same shape and leading dimension")
+    if in_collision is None:
+        in_collision = torch.empty(E, dtype=torch.uint8, device=qa.device)
+    if want_hit_index and hit_index is None:
+        hit_index = torch.empty(E, dtype=torch.int32, device=qa.device)
+    need = L.fastron_edge_workspace_bytes(E, ns, r.n_cp)
+    if workspace is None or workspace.numel() < need:
+        workspace = _workspace(need, qa.device)
+    lds = spos.stride(0) // 4 if ns > 0 else 0
+    _check(L.fastron_edge_check(ctypes.byref(r), _ptr(qa), _ptr(qb), E, qa.stride(0), int(n_interp),
+                                _ptr(spos) if ns else None, _ptr(alpha) if ns else None, ns, lds, _kernel(kind, gamma),
+                                _ptr(in_collision), _ptr(hit_index), _ptr(workspace), workspace.numel(),
+                                _stream(stream)))
+    return in_collision, hit_index
+
+
+def fastron_query(robot, q, spos, alpha, kind: int, gamma: float, score=None, label=None, workspace=None,
+                  stream=None):
+    """FK + score; q / score / label may be host (CPU, ideally pinned) or device tensors."""
+    import torch
+    L = load_library()
+    _require_cuda(spos, alpha)
+    r = robot if isinstance(robot, fastron_robot) else make_robot_struct(robot)
+    nq = q.shape[0]
+    ns = spos.shape[1]
+    need = L.fastron_query_workspace_bytes(nq, ns, r.n_cp, r.dof)
+    if workspace is None or workspace.numel() < need:
+        workspace = _workspace(need, spos.device)
+    lds = spos.stride(0) // 4 if ns > 0 else 0
+    _check(L.fastron_query(ctypes.byref(r), _ptr(q), nq, q.stride(0), _ptr(spos) if ns else None,
+                           _ptr(alpha) if ns else None, ns, lds, _kernel(kind, gamma), _ptr(score), _ptr(label),
+                           _ptr(workspace), workspace.numel(), _stream(stream)))
+    return score, label
+
+
+def launch_count() -> int:
+    return int(load_library().fastron_launch_count())
+
+
+def version() -> str:
+    return load_library().fastron_version().decode()

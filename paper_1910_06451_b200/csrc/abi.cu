@@ -1,0 +1,492 @@
+// abi.cu — the C ABI of include/fastron.h: argument validation, status codes,
+// workspace carving and kernel selection. No computation happens on the host except
+// the per-call robot constants (cos/sin of the fixed D-H twist angles, the pre-scale
+// constant); every step of the hot path runs in the kernels of fk.cu / score.cu /
+// gram.cu / train.cu.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/fastron.h"
+#include "fastron_device.cuh"
+#include "internal.h"
+
+namespace fastron {
+
+std::atomic<int64_t> g_launches{0};
+
+const DeviceInfo& device_info() {
+  static DeviceInfo infos[64];
+  static bool ready[64] = {};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  std::lock_guard<std::mutex> g(mu);
+  if (!ready[dev]) {
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, dev) == cudaSuccess) {
+      infos[dev] = DeviceInfo{dev, p.multiProcessorCount, (int)p.sharedMemPerBlockOptin};
+    } else {
+      infos[dev] = DeviceInfo{dev, 148, 227 * 1024};
+    }
+    ready[dev] = true;
+  }
+  return infos[dev];
+}
+
+}  // namespace fastron
+
+using namespace fastron;
+
+namespace {
+
+thread_local std::string t_last_error;
+
+fastron_status fail(fastron_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  t_last_error = buf;
+  return s;
+}
+
+fastron_status cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return FASTRON_OK;
+  return fail(FASTRON_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define FASTRON_REQUIRE(cond, ...) \
+  do {                             \
+    if (!(cond)) return fail(FASTRON_ERR_INVALID_ARG, __VA_ARGS__); \
+  } while (0)
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+fastron_status check_kernel(const fastron_kernel& k) {
+  FASTRON_REQUIRE(k.kind == FASTRON_RBF_GAUSSIAN || k.kind == FASTRON_RBF_RQ, "kernel kind %d is not a fastron_rbf", k.kind);
+  FASTRON_REQUIRE(std::isfinite(k.gamma) && k.gamma > 0.0f, "gamma must be finite and > 0 (PAPER.md:118), got %g",
+                  (double)k.gamma);
+  return FASTRON_OK;
+}
+
+// Pre-scale so that the kernels evaluate 2^-(c d)^2 = exp(-gamma d^2) (Gaussian) or
+// 1/(1 + (c d)^2)^2 = (1 + gamma/2 d^2)^-2 (RQ, Eq. 3).
+float kernel_scale(const fastron_kernel& k) {
+  const double g = (double)k.gamma;
+  const double c = k.kind == FASTRON_RBF_GAUSSIAN ? std::sqrt(g * 1.4426950408889634074) : std::sqrt(0.5 * g);
+  return (float)c;
+}
+
+fastron_status check_robot(const fastron_robot* r) {
+  FASTRON_REQUIRE(r != nullptr, "robot is NULL");
+  FASTRON_REQUIRE(r->dof >= 1 && r->dof <= FASTRON_MAX_DOF, "dof must be in [1,16], got %d", r->dof);
+  FASTRON_REQUIRE(r->n_cp >= 1 && r->n_cp <= FASTRON_MAX_CP, "n_cp must be in [1,32], got %d", r->n_cp);
+  for (int i = 0; i < r->dof; ++i)
+    for (int c = 0; c < 4; ++c) FASTRON_REQUIRE(std::isfinite(r->dh[i][c]), "dh[%d][%d] is not finite", i, c);
+  for (int i = 0; i < 3; ++i)
+    for (int c = 0; c < 4; ++c) FASTRON_REQUIRE(std::isfinite(r->base[i][c]), "base[%d][%d] is not finite", i, c);
+  for (int m = 0; m < r->n_cp; ++m) {
+    FASTRON_REQUIRE(r->cp_frame[m] >= 0 && r->cp_frame[m] <= r->dof, "cp_frame[%d] = %d outside [0, dof]", m,
+                    r->cp_frame[m]);
+    for (int c = 0; c < 3; ++c) FASTRON_REQUIRE(std::isfinite(r->cp_offset[m][c]), "cp_offset[%d][%d] is not finite", m, c);
+  }
+  return FASTRON_OK;
+}
+
+FkParams make_fk_params(const fastron_robot& r) {
+  FkParams P;
+  memset(&P, 0, sizeof(P));
+  P.dof = r.dof;
+  P.n_cp = r.n_cp;
+  for (int i = 0; i < r.dof; ++i) {
+    P.theta_off[i] = (double)r.dh[i][0];
+    P.d[i] = (double)r.dh[i][1];
+    P.a[i] = (double)r.dh[i][2];
+    P.ca[i] = std::cos((double)r.dh[i][3]);
+    P.sa[i] = std::sin((double)r.dh[i][3]);
+  }
+  for (int c = 0; c < 3; ++c) {
+    for (int rr = 0; rr < 3; ++rr) P.base_c[c][rr] = (double)r.base[rr][c];
+    P.base_p[c] = (double)r.base[c][3];
+  }
+  int n = 0;
+  for (int j = 0; j <= r.dof; ++j) {
+    P.frame_begin[j] = n;
+    for (int m = 0; m < r.n_cp; ++m)
+      if (r.cp_frame[m] == j) P.frame_list[n++] = m;
+  }
+  for (int j = r.dof + 1; j <= FASTRON_MAX_DOF; ++j) P.frame_begin[j] = n;
+  for (int m = 0; m < r.n_cp; ++m)
+    for (int c = 0; c < 3; ++c) P.cp_off[m][c] = (double)r.cp_offset[m][c];
+  return P;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+constexpr int64_t kQueryChunk = 1 << 18;  // queries per pipelined chunk of fastron_query
+
+// One non-blocking copy stream per device for fastron_query's host<->device pipeline.
+cudaStream_t query_copy_stream() {
+  static cudaStream_t streams[64] = {};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+  return streams[dev];
+}
+
+bool is_host_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeUnregistered;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fastron_last_error(void) { return t_last_error.c_str(); }
+
+const char* fastron_version(void) { return "fastron_b200 0.1.0 (sm_100a)"; }
+
+int64_t fastron_launch_count(void) { return g_launches.load(); }
+
+fastron_status fastron_fk(const fastron_robot* robot, const float* q, int64_t n, int64_t ldq, float* pos, int64_t ldpos,
+                          void* stream) {
+  fastron_status s = check_robot(robot);
+  if (s != FASTRON_OK) return s;
+  FASTRON_REQUIRE(n >= 0, "n must be >= 0");
+  if (n == 0) return FASTRON_OK;
+  FASTRON_REQUIRE(q && pos, "q and pos must be non-NULL");
+  FASTRON_REQUIRE(ldq >= robot->dof, "ldq (%lld) < dof (%d)", (long long)ldq, robot->dof);
+  FASTRON_REQUIRE(ldpos >= n, "ldpos (%lld) < n (%lld)", (long long)ldpos, (long long)n);
+  FASTRON_REQUIRE(((uintptr_t)pos & 15) == 0, "pos must be 16-byte aligned");
+  return cuda_status(launch_fk(make_fk_params(*robot), q, n, ldq, reinterpret_cast<float4*>(pos), ldpos, S(stream)),
+                     "fastron_fk");
+}
+
+size_t fastron_score_workspace_bytes(int64_t nq, int64_t ns, int32_t n_cp) {
+  if (nq < 0 || ns < 0 || n_cp < 1 || n_cp > FASTRON_MAX_CP) return 0;
+  return align_up(packed_bytes(ns, n_cp)) + align_up(score_partial_bytes(nq, ns, n_cp));
+}
+
+fastron_status fastron_score(const float* qpos, int64_t nq, int64_t ldq, const float* spos, const float* alpha,
+                             int64_t ns, int64_t lds, int32_t n_cp, fastron_kernel k, float* score, int8_t* label,
+                             void* workspace, size_t workspace_bytes, void* stream) {
+  fastron_status s = check_kernel(k);
+  if (s != FASTRON_OK) return s;
+  FASTRON_REQUIRE(nq >= 0 && ns >= 0, "nq and ns must be >= 0");
+  FASTRON_REQUIRE(n_cp >= 1 && n_cp <= FASTRON_MAX_CP, "n_cp must be in [1,32], got %d", n_cp);
+  if (nq == 0) return FASTRON_OK;
+  FASTRON_REQUIRE(qpos != nullptr, "qpos is NULL");
+  FASTRON_REQUIRE(ldq >= nq, "ldq (%lld) < nq (%lld)", (long long)ldq, (long long)nq);
+  FASTRON_REQUIRE(score || label, "score and label are both NULL");
+  if (ns > 0) {
+    FASTRON_REQUIRE(spos && alpha, "spos and alpha must be non-NULL when ns > 0");
+    FASTRON_REQUIRE(lds >= ns, "lds (%lld) < ns (%lld)", (long long)lds, (long long)ns);
+  }
+  const size_t need = fastron_score_workspace_bytes(nq, ns, n_cp);
+  if (workspace_bytes < need || (need > 0 && !workspace))
+    return fail(FASTRON_ERR_WORKSPACE, "fastron_score needs %zu workspace bytes, got %zu", need, workspace_bytes);
+  FASTRON_REQUIRE(((uintptr_t)workspace & 255) == 0, "workspace must be 256-byte aligned");
+  char* ws = static_cast<char*>(workspace);
+  float* packed = reinterpret_cast<float*>(ws);
+  double* partial = reinterpret_cast<double*>(ws + align_up(packed_bytes(ns, n_cp)));
+  const float c = kernel_scale(k);
+  cudaError_t e = launch_pack(reinterpret_cast<const float4*>(spos), lds, alpha, ns, n_cp, c, packed, S(stream));
+  if (e != cudaSuccess) return cuda_status(e, "fastron_score(pack)");
+  e = launch_score(reinterpret_cast<const float4*>(qpos), nq, ldq, packed, ns, n_cp, k.kind, c, score, label, partial,
+                   S(stream));
+  return cuda_status(e, "fastron_score");
+}
+
+size_t fastron_model_bytes(int64_t ns, int32_t n_cp) {
+  if (ns < 0 || n_cp < 1 || n_cp > FASTRON_MAX_CP) return 0;
+  return align_up(packed_bytes(ns, n_cp));
+}
+
+fastron_status fastron_model_pack(const float* spos, const float* alpha, int64_t ns, int64_t lds, int32_t n_cp,
+                                  fastron_kernel k, void* packed, size_t packed_bytes_given, void* stream) {
+  fastron_status s = check_kernel(k);
+  if (s != FASTRON_OK) return s;
+  FASTRON_REQUIRE(ns >= 0, "ns must be >= 0");
+  FASTRON_REQUIRE(n_cp >= 1 && n_cp <= FASTRON_MAX_CP, "n_cp must be in [1,32], got %d", n_cp);
+  if (ns == 0) return FASTRON_OK;
+  FASTRON_REQUIRE(spos && alpha, "spos and alpha must be non-NULL when ns > 0");
+  FASTRON_REQUIRE(lds >= ns, "lds (%lld) < ns (%lld)", (long long)lds, (long long)ns);
+  const size_t need = fastron_model_bytes(ns, n_cp);
+  if (packed_bytes_given < need || !packed)
+    return fail(FASTRON_ERR_WORKSPACE, "fastron_model_pack needs %zu bytes, got %zu", need, packed_bytes_given);
+  FASTRON_REQUIRE(((uintptr_t)packed & 255) == 0, "packed must be 256-byte aligned");
+  return cuda_status(launch_pack(reinterpret_cast<const float4*>(spos), lds, alpha, ns, n_cp, kernel_scale(k),
+                                 static_cast<float*>(packed), S(stream)),
+                     "fastron_model_pack");
+}
+
+size_t fastron_score_packed_workspace_bytes(int64_t nq, int64_t ns, int32_t n_cp) {
+  if (nq < 0 || ns < 0 || n_cp < 1 || n_cp > FASTRON_MAX_CP) return 0;
+  return align_up(score_partial_bytes(nq, ns, n_cp));
+}
+
+fastron_status fastron_score_packed(const float* qpos, int64_t nq, int64_t ldq, const void* packed, int64_t ns,
+                                    int32_t n_cp, fastron_kernel k, float* score, int8_t* label, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
+  fastron_status s = check_kernel(k);
+  if (s != FASTRON_OK) return s;
+  FASTRON_REQUIRE(nq >= 0 && ns >= 0, "nq and ns must be >= 0");
+  FASTRON_REQUIRE(n_cp >= 1 && n_cp <= FASTRON_MAX_CP, "n_cp must be in [1,32], got %d", n_cp);
+  if (nq == 0) return FASTRON_OK;
+  FASTRON_REQUIRE(qpos != nullptr, "qpos is NULL");
+  FASTRON_REQUIRE(ldq >= nq, "ldq (%lld) < nq (%lld)", (long long)ldq, (long long)nq);
+  FASTRON_REQUIRE(score || label, "score and label are both NULL");
+  FASTRON_REQUIRE(ns == 0 || packed, "packed is NULL");
+  const size_t need = fastron_score_packed_workspace_bytes(nq, ns, n_cp);
+  if (workspace_bytes < need || (need > 0 && !workspace))
+    return fail(FASTRON_ERR_WORKSPACE, "fastron_score_packed needs %zu workspace bytes, got %zu", need,
+                workspace_bytes);
+  return cuda_status(launch_score(reinterpret_cast<const float4*>(qpos), nq, ldq, static_cast<const float*>(packed), ns,
+                                  n_cp, k.kind, kernel_scale(k), score, label, static_cast<double*>(workspace),
+                                  S(stream)),
+                     "fastron_score_packed");
+}
+
+size_t fastron_gram_workspace_bytes(int64_t n, int32_t n_cp) {
+  if (n < 0 || n_cp < 1 || n_cp > FASTRON_MAX_CP) return 0;
+  // the Gram kernel reads column tiles in pairs: round the packed buffer to an even tile count
+  const int64_t tiles = n_support_tiles(n);
+  return align_up(packed_bytes((tiles + 1) / 2 * 2 * kTileSupports, n_cp));
+}
+
+fastron_status fastron_gram(const float* pos, int64_t n, int64_t ldp, int32_t n_cp, fastron_kernel k, float* K,
+                            int64_t ldk, void* workspace, size_t workspace_bytes, void* stream) {
+  fastron_status s = check_kernel(k);
+  if (s != FASTRON_OK) return s;
+  FASTRON_REQUIRE(n >= 0, "n must be >= 0");
+  FASTRON_REQUIRE(n_cp >= 1 && n_cp <= FASTRON_MAX_CP, "n_cp must be in [1,32], got %d", n_cp);
+  if (n == 0) return FASTRON_OK;
+  FASTRON_REQUIRE(pos && K, "pos and K must be non-NULL");
+  FASTRON_REQUIRE(ldp >= n && ldk >= n, "ldp and ldk must be >= n");
+  const size_t need = fastron_gram_workspace_bytes(n, n_cp);
+  if (workspace_bytes < need || !workspace)
+    return fail(FASTRON_ERR_WORKSPACE, "fastron_gram needs %zu workspace bytes, got %zu", need, workspace_bytes);
+  FASTRON_REQUIRE(((uintptr_t)workspace & 255) == 0, "workspace must be 256-byte aligned");
+  float* packed = static_cast<float*>(workspace);
+  const float c = kernel_scale(k);
+  cudaError_t e = launch_pack(reinterpret_cast<const float4*>(pos), ldp, nullptr, n, n_cp, c, packed, S(stream));
+  if (e != cudaSuccess) return cuda_status(e, "fastron_gram(pack)");
+  return cuda_status(launch_gram(packed, n, n_cp, k.kind, K, ldk, S(stream)), "fastron_gram");
+}
+
+int64_t fastron_train_max_n(void) { return train_max_n(); }
+
+fastron_status fastron_train(const float* K, int64_t n, int64_t ldk, const int8_t* y, double beta, int64_t iter_max,
+                             int64_t s_max, double* alpha_inout, double* F_inout, int32_t* support_idx, int32_t* trace,
+                             fastron_train_result* result, void* stream) {
+  FASTRON_REQUIRE(n >= 0 && iter_max >= 0 && s_max >= 0, "n, iter_max and s_max must be >= 0");
+  FASTRON_REQUIRE(std::isfinite(beta) && beta >= 1.0, "beta must be >= 1 (PAPER.md:189), got %g", beta);
+  FASTRON_REQUIRE(result != nullptr, "result is NULL");
+  if (n > fastron_train_max_n())
+    return fail(FASTRON_ERR_UNSUPPORTED, "n = %lld exceeds fastron_train_max_n() = %lld", (long long)n,
+                (long long)fastron_train_max_n());
+  if (n > 0x7fffffffLL) return fail(FASTRON_ERR_UNSUPPORTED, "n too large");
+  if (n == 0) return cuda_status(cudaMemsetAsync(result, 0, sizeof(*result), S(stream)), "fastron_train");
+  FASTRON_REQUIRE(K && y && alpha_inout && F_inout, "K, y, alpha_inout and F_inout must be non-NULL");
+  FASTRON_REQUIRE(ldk >= n, "ldk (%lld) < n (%lld)", (long long)ldk, (long long)n);
+  return cuda_status(launch_train(K, n, ldk, y, beta, iter_max, s_max, alpha_inout, F_inout, support_idx, trace, result,
+                                  S(stream)),
+                     "fastron_train");
+}
+
+size_t fastron_edge_workspace_bytes(int64_t n_edges, int64_t ns, int32_t n_cp) {
+  if (n_edges < 0 || ns < 0 || n_cp < 1 || n_cp > FASTRON_MAX_CP) return 0;
+  const size_t lists = 2 * align_up((size_t)n_edges * 4) + 256;  // two active lists + two counters
+  return align_up(packed_bytes(ns, n_cp)) + align_up(score_partial_bytes(n_edges * 32, ns, n_cp)) + lists;
+}
+
+fastron_status fastron_edge_check(const fastron_robot* robot, const float* qa, const float* qb, int64_t n_edges,
+                                  int64_t ldq, int32_t n_interp, const float* spos, const float* alpha, int64_t ns,
+                                  int64_t lds, fastron_kernel k, uint8_t* in_collision, int32_t* hit_index,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+  fastron_status s = check_robot(robot);
+  if (s != FASTRON_OK) return s;
+  s = check_kernel(k);
+  if (s != FASTRON_OK) return s;
+  FASTRON_REQUIRE(n_edges >= 0 && ns >= 0, "n_edges and ns must be >= 0");
+  FASTRON_REQUIRE(n_interp >= 1, "n_interp must be >= 1, got %d", n_interp);
+  if (n_edges == 0) return FASTRON_OK;
+  FASTRON_REQUIRE(n_edges <= (int64_t)1 << 26, "n_edges too large for one call (max 2^26)");
+  FASTRON_REQUIRE(qa && qb && in_collision, "qa, qb and in_collision must be non-NULL");
+  FASTRON_REQUIRE(ldq >= robot->dof, "ldq (%lld) < dof (%d)", (long long)ldq, robot->dof);
+  if (ns > 0) {
+    FASTRON_REQUIRE(spos && alpha, "spos and alpha must be non-NULL when ns > 0");
+    FASTRON_REQUIRE(lds >= ns, "lds (%lld) < ns (%lld)", (long long)lds, (long long)ns);
+  }
+  const size_t need = fastron_edge_workspace_bytes(n_edges, ns, robot->n_cp);
+  if (workspace_bytes < need || !workspace)
+    return fail(FASTRON_ERR_WORKSPACE, "fastron_edge_check needs %zu workspace bytes, got %zu", need, workspace_bytes);
+  FASTRON_REQUIRE(((uintptr_t)workspace & 255) == 0, "workspace must be 256-byte aligned");
+  const int M = robot->n_cp;
+  char* ws = static_cast<char*>(workspace);
+  float* packed = reinterpret_cast<float*>(ws);
+  ws += align_up(packed_bytes(ns, M));
+  double* partial = reinterpret_cast<double*>(ws);
+  ws += align_up(score_partial_bytes(n_edges * 32, ns, M));
+  int32_t* counts = reinterpret_cast<int32_t*>(ws);  // [2] live counters (256 B reserved)
+  ws += 256;
+  int32_t* lists[2] = {reinterpret_cast<int32_t*>(ws), reinterpret_cast<int32_t*>(ws + align_up((size_t)n_edges * 4))};
+  const float c = kernel_scale(k);
+  cudaStream_t st = S(stream);
+  cudaError_t e = launch_pack(reinterpret_cast<const float4*>(spos), lds, alpha, ns, M, c, packed, st);
+  if (e != cudaSuccess) return cuda_status(e, "fastron_edge_check(pack)");
+  const FkParams P = make_fk_params(*robot);
+  const int rounds = (n_interp + 31) / 32;
+  for (int r = 0; r < rounds; ++r) {
+    EdgeRound R;
+    R.qa = qa;
+    R.qb = qb;
+    R.ldq = ldq;
+    R.n_edges = n_edges;
+    R.n_interp = n_interp;
+    R.round = r;
+    R.active = r == 0 ? nullptr : lists[(r - 1) & 1];
+    R.active_count = r == 0 ? nullptr : counts + ((r - 1) & 1);
+    R.next_active = lists[r & 1];
+    R.next_count = counts + (r & 1);
+    R.in_collision = in_collision;
+    R.hit_index = hit_index;
+    e = cudaMemsetAsync(R.next_count, 0, sizeof(int32_t), st);
+    if (e != cudaSuccess) return cuda_status(e, "fastron_edge_check(memset)");
+    e = launch_edge_round(P, R, packed, ns, M, k.kind, c, partial, st);
+    if (e != cudaSuccess) return cuda_status(e, "fastron_edge_check");
+  }
+  return FASTRON_OK;
+}
+
+size_t fastron_query_workspace_bytes(int64_t nq, int64_t ns, int32_t n_cp, int32_t dof) {
+  if (nq < 0 || ns < 0 || n_cp < 1 || n_cp > FASTRON_MAX_CP || dof < 1 || dof > FASTRON_MAX_DOF) return 0;
+  const int64_t chunk = nq < kQueryChunk ? nq : kQueryChunk;
+  // per in-flight chunk: q (dof floats), positions (n_cp float4), score (float), label (int8); two chunks
+  const size_t per = align_up((size_t)chunk * dof * 4) + align_up((size_t)chunk * n_cp * 16) +
+                     align_up((size_t)chunk * 4) + align_up((size_t)chunk);
+  return align_up(packed_bytes(ns, n_cp)) + align_up(score_partial_bytes(chunk, ns, n_cp)) + 2 * per;
+}
+
+fastron_status fastron_query(const fastron_robot* robot, const float* q, int64_t nq, int64_t ldq, const float* spos,
+                             const float* alpha, int64_t ns, int64_t lds, fastron_kernel k, float* score,
+                             int8_t* label, void* workspace, size_t workspace_bytes, void* stream) {
+  fastron_status s = check_robot(robot);
+  if (s != FASTRON_OK) return s;
+  s = check_kernel(k);
+  if (s != FASTRON_OK) return s;
+  FASTRON_REQUIRE(nq >= 0 && ns >= 0, "nq and ns must be >= 0");
+  if (nq == 0) return FASTRON_OK;
+  FASTRON_REQUIRE(q != nullptr, "q is NULL");
+  FASTRON_REQUIRE(score || label, "score and label are both NULL");
+  FASTRON_REQUIRE(ldq >= robot->dof, "ldq (%lld) < dof (%d)", (long long)ldq, robot->dof);
+  if (ns > 0) {
+    FASTRON_REQUIRE(spos && alpha, "spos and alpha must be non-NULL when ns > 0");
+    FASTRON_REQUIRE(lds >= ns, "lds (%lld) < ns (%lld)", (long long)lds, (long long)ns);
+  }
+  const int M = robot->n_cp, D = robot->dof;
+  const size_t need = fastron_query_workspace_bytes(nq, ns, M, D);
+  if (workspace_bytes < need || !workspace)
+    return fail(FASTRON_ERR_WORKSPACE, "fastron_query needs %zu workspace bytes, got %zu", need, workspace_bytes);
+  FASTRON_REQUIRE(((uintptr_t)workspace & 255) == 0, "workspace must be 256-byte aligned");
+  const bool q_host = is_host_ptr(q), s_host = is_host_ptr(score), l_host = is_host_ptr(label);
+  const int64_t chunk = nq < kQueryChunk ? nq : kQueryChunk;
+  char* ws = static_cast<char*>(workspace);
+  float* packed = reinterpret_cast<float*>(ws);
+  ws += align_up(packed_bytes(ns, M));
+  double* partial = reinterpret_cast<double*>(ws);
+  ws += align_up(score_partial_bytes(chunk, ns, M));
+  struct Buf { float* q; float* pos; float* sc; int8_t* lb; } buf[2];
+  for (int b = 0; b < 2; ++b) {
+    buf[b].q = reinterpret_cast<float*>(ws); ws += align_up((size_t)chunk * D * 4);
+    buf[b].pos = reinterpret_cast<float*>(ws); ws += align_up((size_t)chunk * M * 16);
+    buf[b].sc = reinterpret_cast<float*>(ws); ws += align_up((size_t)chunk * 4);
+    buf[b].lb = reinterpret_cast<int8_t*>(ws); ws += align_up((size_t)chunk);
+  }
+  cudaStream_t st = S(stream);
+  const float c = kernel_scale(k);
+  const FkParams P = make_fk_params(*robot);
+  cudaError_t e = launch_pack(reinterpret_cast<const float4*>(spos), lds, alpha, ns, M, c, packed, st);
+  if (e != cudaSuccess) return cuda_status(e, "fastron_query(pack)");
+  const bool any_host = q_host || s_host || l_host;
+  if (!any_host) {
+    // device pointers: FK of the whole batch through the positions buffer in chunks
+    for (int64_t off = 0; off < nq; off += chunk) {
+      const int64_t n = nq - off < chunk ? nq - off : chunk;
+      e = launch_fk(P, q + off * ldq, n, ldq, reinterpret_cast<float4*>(buf[0].pos), chunk, st);
+      if (e == cudaSuccess)
+        e = launch_score(reinterpret_cast<const float4*>(buf[0].pos), n, chunk, packed, ns, M, k.kind, c,
+                         score ? score + off : nullptr, label ? label + off : nullptr, partial, st);
+      if (e != cudaSuccess) return cuda_status(e, "fastron_query");
+    }
+    return FASTRON_OK;
+  }
+  // host buffers: H2D(chunk c+1) on a copy stream overlaps FK+score(chunk c) on `stream`
+  cudaStream_t cp = query_copy_stream();
+  cudaEvent_t ev_in[2], ev_done[2], ev_out[2];
+  for (int b = 0; b < 2; ++b) {
+    cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_done[b], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_out[b], cudaEventDisableTiming);
+  }
+  cudaEventRecord(ev_out[0], st);
+  cudaEventRecord(ev_out[1], st);
+  int64_t idx = 0;
+  for (int64_t off = 0; off < nq && e == cudaSuccess; off += chunk, ++idx) {
+    const int b = (int)(idx & 1);
+    const int64_t n = nq - off < chunk ? nq - off : chunk;
+    // stage q: the buffer is free once the previous use of it has been copied out
+    cudaStreamWaitEvent(cp, ev_out[b], 0);
+    const float* qsrc = q + off * ldq;
+    float* qdev = q_host ? buf[b].q : const_cast<float*>(qsrc);
+    int64_t ldq_dev = q_host ? D : ldq;
+    if (q_host) {
+      if (ldq == D) e = cudaMemcpyAsync(qdev, qsrc, (size_t)n * D * 4, cudaMemcpyHostToDevice, cp);
+      else e = cudaMemcpy2DAsync(qdev, (size_t)D * 4, qsrc, (size_t)ldq * 4, (size_t)D * 4, (size_t)n,
+                                 cudaMemcpyHostToDevice, cp);
+    }
+    cudaEventRecord(ev_in[b], cp);
+    cudaStreamWaitEvent(st, ev_in[b], 0);
+    float* sdev = score ? (s_host ? buf[b].sc : score + off) : nullptr;
+    int8_t* ldev = label ? (l_host ? buf[b].lb : label + off) : nullptr;
+    if (e == cudaSuccess) e = launch_fk(P, qdev, n, ldq_dev, reinterpret_cast<float4*>(buf[b].pos), chunk, st);
+    if (e == cudaSuccess)
+      e = launch_score(reinterpret_cast<const float4*>(buf[b].pos), n, chunk, packed, ns, M, k.kind, c, sdev, ldev,
+                       partial, st);
+    cudaEventRecord(ev_done[b], st);
+    cudaStreamWaitEvent(cp, ev_done[b], 0);
+    if (e == cudaSuccess && score && s_host) e = cudaMemcpyAsync(score + off, sdev, (size_t)n * 4, cudaMemcpyDeviceToHost, cp);
+    if (e == cudaSuccess && label && l_host) e = cudaMemcpyAsync(label + off, ldev, (size_t)n, cudaMemcpyDeviceToHost, cp);
+    cudaEventRecord(ev_out[b], cp);
+    cudaStreamWaitEvent(st, ev_out[b], 0);
+  }
+  cudaError_t e2 = cudaStreamSynchronize(cp);
+  cudaError_t e3 = cudaStreamSynchronize(st);
+  for (int b = 0; b < 2; ++b) {
+    cudaEventDestroy(ev_in[b]);
+    cudaEventDestroy(ev_done[b]);
+    cudaEventDestroy(ev_out[b]);
+  }
+  if (e == cudaSuccess) e = e2;
+  if (e == cudaSuccess) e = e3;
+  return cuda_status(e, "fastron_query");
+}
+
+}  // extern "C"

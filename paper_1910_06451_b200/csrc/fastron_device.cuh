@@ -1,0 +1,150 @@
+// fastron_device.cuh — device building blocks shared by the sm_100a kernels of the
+// Fastron FK hot path: packed-f32x2 arithmetic, the per-control-point RBF term,
+// the support-tile layout, mbarrier + cp.async.bulk (TMA bulk copy) helpers.
+//
+// The FK-kernel term (Eq. 4) is evaluated on PAIRS of control
+// points (m, m+1) with the packed FP32 pipe (FADD2/FMUL2/FFMA2) and one MUFU op per
+// control point: ex2.approx (Gaussian, north star) or rcp.approx (RQ, Eq. 3,
+// PAPER.md:115-117). Positions are pre-scaled so that
+//   Gaussian: exp(-gamma d^2) = 2^-(c d)^2,   c = sqrt(gamma log2 e)
+//   RQ:       (1 + gamma/2 d^2)^-2 = 1 / (1 + (c d)^2)^2,   c = sqrt(gamma / 2).
+// Every kernel that evaluates K_FK (score, Gram, edge) calls term_pair() below with
+// identically scaled fp32 inputs, so the same (q, s) pair yields the same bits
+// everywhere ("one term function").
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fastron {
+
+constexpr int kGaussian = 0;
+constexpr int kRQ = 1;
+
+// Support tile: TS supports per tile. Each support is MP/2 pair records of 8 floats
+// (x_m, x_m+1, y_m, y_m+1, z_m, z_m+1, 0, 0), pre-scaled, followed after the TS
+// records by TS alpha values. Padded control points (m >= M) hold kPadCoord so their
+// term is exactly 0; padded supports (index >= ns) hold zeros and alpha = 0.
+constexpr int kTileSupports = 64;
+constexpr float kPadCoord = 1.0e30f;
+
+__host__ __device__ constexpr int pair_floats() { return 8; }
+__host__ __device__ constexpr int64_t tile_floats(int mp) { return (int64_t)kTileSupports * (mp / 2) * 8 + kTileSupports; }
+__host__ __device__ constexpr int64_t tile_bytes(int mp) { return tile_floats(mp) * 4; }
+
+// ---------------------------------------------------------------------------------
+// packed f32x2 helpers (PTX .f32x2, sm_100a): one instruction, two IEEE rn results
+// ---------------------------------------------------------------------------------
+typedef unsigned long long f2;
+
+__device__ __forceinline__ f2 pk(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float lo(f2 v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  (void)b;
+  return a;
+}
+__device__ __forceinline__ float hi(f2 v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  (void)a;
+  return b;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ float ex2_neg(float x) {  // 2^-x on the MUFU (source negation is free)
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-x));
+  return r;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// The RBF terms of control points (m, m+1) for one (query, support) pair.
+// Gaussian: d2 = dx*dx; d2 = fma(dy,dy,d2); d2 = fma(dz,dz,d2); t = 2^-d2
+// RQ:       w = fma(dx,dx,1); w = fma(dy,dy,w); w = fma(dz,dz,w); t = rcp(w*w)
+template <int KIND>
+__device__ __forceinline__ f2 term_pair(f2 ux, f2 uy, f2 uz, f2 vx, f2 vy, f2 vz) {
+  f2 dx = sub2(ux, vx);
+  f2 dy = sub2(uy, vy);
+  f2 dz = sub2(uz, vz);
+  if (KIND == kGaussian) {
+    f2 s = mul2(dx, dx);
+    s = fma2(dy, dy, s);
+    s = fma2(dz, dz, s);
+    return pk(ex2_neg(lo(s)), ex2_neg(hi(s)));
+  } else {
+    const f2 one = pk(1.0f, 1.0f);
+    f2 w = fma2(dx, dx, one);
+    w = fma2(dy, dy, w);
+    w = fma2(dz, dz, w);
+    w = mul2(w, w);
+    return pk(rcp_approx(lo(w)), rcp_approx(hi(w)));
+  }
+}
+
+// Sum over the M control points of one (query, support) pair, in the fixed order
+// (t0 + t2 + t4 + ...) + (t1 + t3 + ...): the canonical K_FK numerator shared by all kernels.
+__device__ __forceinline__ float pair_sum(f2 acc) { return lo(acc) + hi(acc); }
+
+// ---------------------------------------------------------------------------------
+// mbarrier + TMA bulk copy (cp.async.bulk global -> shared), CTA scope
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(phase)
+      : "memory");
+}
+
+}  // namespace fastron

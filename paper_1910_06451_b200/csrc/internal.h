@@ -1,0 +1,76 @@
+// internal.h — host-side launchers of the sm_100a kernels (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+
+#include "fk_device.cuh"
+
+namespace fastron {
+
+extern std::atomic<int64_t> g_launches;  // kernels launched by this process (bench gpu_launches)
+
+struct DeviceInfo {
+  int device;
+  int sms;
+  int max_smem_optin;
+};
+const DeviceInfo& device_info();
+
+// K1: control-point positions, float4 [M][ldpos]
+cudaError_t launch_fk(const FkParams& P, const float* q, int64_t n, int64_t ldq, float4* pos, int64_t ldpos,
+                      cudaStream_t st);
+
+// Padded, scaled support tiles (see fastron_device.cuh for the layout).
+int padded_m(int M);
+int64_t n_support_tiles(int64_t ns);
+size_t packed_bytes(int64_t ns, int M);
+cudaError_t launch_pack(const float4* spos, int64_t lds, const float* alpha, int64_t ns, int M, float scale,
+                        float* packed, cudaStream_t st);
+
+// K2: scoring. Plan = grid decomposition (query blocks x support splits).
+struct ScorePlan {
+  int64_t n_qblocks;
+  int32_t n_splits;
+  int32_t tiles_per_split;
+  int64_t n_tiles;
+};
+int score_queries_per_cta(int M);
+int score_max_splits(int64_t nq, int64_t ns, int M);
+ScorePlan plan_score(int64_t nq, int64_t ns, int M, int kind);
+size_t score_partial_bytes(int64_t nq, int64_t ns, int M);
+
+cudaError_t launch_score(const float4* qpos, int64_t nq, int64_t ldq, const float* packed, int64_t ns, int M, int kind,
+                         float scale, float* score, int8_t* label, double* partial, cudaStream_t st);
+
+// K4: one round of the fused edge check (interpolate -> FK -> score -> warp vote).
+struct EdgeRound {
+  const float* qa;
+  const float* qb;
+  int64_t ldq;
+  int64_t n_edges;
+  int32_t n_interp;
+  int32_t round;
+  const int32_t* active;  // round > 0: edges still undecided
+  const int32_t* active_count;
+  int32_t* next_active;
+  int32_t* next_count;
+  uint8_t* in_collision;
+  int32_t* hit_index;
+};
+cudaError_t launch_edge_round(const FkParams& P, const EdgeRound& R, const float* packed, int64_t ns, int M, int kind,
+                              float scale, double* partial, cudaStream_t st);
+
+// K3: Gram
+cudaError_t launch_gram(const float* packed, int64_t n, int M, int kind, float* K, int64_t ldk, cudaStream_t st);
+
+// K5: Algorithm 1
+struct TrainOut;
+int64_t train_max_n();
+cudaError_t launch_train(const float* K, int64_t n, int64_t ldk, const int8_t* y, double beta, int64_t iter_max,
+                         int64_t s_max, double* alpha, double* F, int32_t* support_idx, int32_t* trace, void* result,
+                         cudaStream_t st);
+
+}  // namespace fastron

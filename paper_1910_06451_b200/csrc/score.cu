@@ -1,0 +1,465 @@
+// score.cu — K2, Fastron scoring f(x) = sum_i alpha_i K_FK(S_i, x) with
+// K_FK of Eq. 4, plus the fused edge-check rounds (K4) that reuse
+// the same support-streaming loop with an interpolate+FK prologue and a warp-vote
+// epilogue.
+//
+// Design:
+//  * The support set is first packed once per call into tiles of 64 supports
+//    (pre-scaled, control points paired (m, m+1), alpha appended), so one
+//    cp.async.bulk (TMA bulk copy) moves a whole tile into shared memory; a
+//    3-stage mbarrier ring overlaps the next tiles' copies with compute.
+//  * Each thread owns QT queries whose scaled control points live in registers as
+//    f32x2 pairs; every support record is a warp-broadcast LDS.128 + LDS.64 shared
+//    by the QT queries. Per control-point pair: 3 FADD2 + FMUL2 + 2 FFMA2 +
+//    2 MUFU (ex2 or rcp) + FADD2 — MUFU-bound (one SFU op per term).
+//  * Accumulation: per support the M terms are summed in fp32 (fixed order), the
+//    alpha-weighted sum of 8 supports is an fp32 FFMA chain, folded into an fp64
+//    accumulator per query (DESIGN.md §5 error budget). 1/M is applied once at the
+//    end in fp64.
+//  * Grid = query blocks x support splits, the split count chosen to fill 148 SMs in
+//    whole waves; splits > 1 write fp64 partials that a second kernel adds in a fixed
+//    order (deterministic).
+#include "fastron_device.cuh"
+#include "internal.h"
+
+namespace fastron {
+
+constexpr int kNT = 128;     // threads per scoring CTA
+constexpr int kStages = 3;   // TMA ring depth
+constexpr int kGroup = 8;    // supports per fp32 partial before the fp64 fold
+
+__host__ __device__ constexpr int qt_for(int mp) { return mp <= 4 ? 8 : mp <= 8 ? 4 : mp <= 16 ? 2 : 1; }
+
+int padded_m(int M) { return (M + 1) & ~1; }
+int64_t n_support_tiles(int64_t ns) { return (ns + kTileSupports - 1) / kTileSupports; }
+size_t packed_bytes(int64_t ns, int M) { return (size_t)n_support_tiles(ns) * (size_t)tile_bytes(padded_m(M)); }
+int score_queries_per_cta(int M) { return kNT * qt_for(padded_m(M)); }
+
+// ---------------------------------------------------------------------------------
+// pack: spos float4 [M][lds] + alpha -> scaled, paired tiles
+// ---------------------------------------------------------------------------------
+__global__ void pack_kernel(const float4* __restrict__ spos, int64_t lds, const float* __restrict__ alpha, int64_t ns,
+                            int M, int MP, float scale, float* __restrict__ packed, int64_t n_slots) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_slots) return;
+  const int64_t tile = i / kTileSupports;
+  const int s = (int)(i % kTileSupports);
+  float* T = packed + tile * tile_floats(MP);
+  float* rec = T + (int64_t)s * (MP / 2) * 8;
+  const bool live = i < ns;
+  for (int p = 0; p < MP / 2; ++p) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    const int m0 = 2 * p, m1 = 2 * p + 1;
+    if (live) a = spos[(int64_t)m0 * lds + i];
+    if (live && m1 < M) b = spos[(int64_t)m1 * lds + i];
+    float ax = __fmul_rn(a.x, scale), ay = __fmul_rn(a.y, scale), az = __fmul_rn(a.z, scale);
+    float bx = __fmul_rn(b.x, scale), by = __fmul_rn(b.y, scale), bz = __fmul_rn(b.z, scale);
+    if (m1 >= M) bx = by = bz = kPadCoord;  // padded control point: term is exactly 0
+    reinterpret_cast<float4*>(rec + p * 8)[0] = make_float4(ax, bx, ay, by);
+    reinterpret_cast<float4*>(rec + p * 8)[1] = make_float4(az, bz, 0.f, 0.f);
+  }
+  T[(int64_t)kTileSupports * (MP / 2) * 8 + s] = (live && alpha) ? alpha[i] : 0.0f;
+}
+
+cudaError_t launch_pack(const float4* spos, int64_t lds, const float* alpha, int64_t ns, int M, float scale,
+                        float* packed, cudaStream_t st) {
+  const int64_t slots = n_support_tiles(ns) * kTileSupports;
+  if (slots == 0) return cudaSuccess;
+  const int threads = 256;
+  pack_kernel<<<(unsigned)((slots + threads - 1) / threads), threads, 0, st>>>(spos, lds, alpha, ns, M, padded_m(M),
+                                                                                 scale, packed, slots);
+  g_launches.fetch_add(1);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------
+// the scoring kernel (positions mode and fused edge mode)
+// ---------------------------------------------------------------------------------
+enum { MODE_POS = 0, MODE_EDGE = 1 };
+
+struct ScoreArgs {
+  const float4* qpos;
+  int64_t ldq;
+  int64_t nq;  // number of (virtual) queries the grid covers
+  const float* packed;
+  int64_t n_tiles;
+  int32_t tiles_per_split;
+  int32_t n_splits;
+  int32_t M;
+  float scale;
+  float* score;
+  int8_t* label;
+  double* partial;
+  // edge mode
+  const float* qa;
+  const float* qb;
+  int64_t ldqe;
+  int32_t n_interp;
+  int32_t round;
+  const int32_t* active;
+  const int32_t* active_count;
+  int32_t* next_active;
+  int32_t* next_count;
+  uint8_t* in_collision;
+  int32_t* hit_index;
+};
+
+// Position k of the visiting order of round r, lane l: evens first, then odds (R11).
+__device__ __forceinline__ int edge_point(int n_interp, int o) {
+  const int n_even = (n_interp + 1) >> 1;
+  return o < n_even ? 2 * o : 2 * (o - n_even) + 1;
+}
+
+__device__ __forceinline__ int64_t edge_active_queries(const ScoreArgs& A) {
+  return A.active_count ? (int64_t)(*A.active_count) * 32 : A.nq;
+}
+
+// Warp vote over the 32 lanes that hold one (edge, round) item; called by full warps.
+__device__ __forceinline__ void edge_vote(const ScoreArgs& A, int64_t vq, double f) {
+  const int lane = threadIdx.x & 31;
+  const int64_t slot = vq >> 5;
+  const int64_t n_active = edge_active_queries(A) >> 5;
+  const bool in_range = slot < n_active;  // warp-uniform
+  const int o = A.round * 32 + lane;
+  const bool valid = in_range && o < A.n_interp;
+  const bool hit = valid && f > 0.0;
+  const unsigned ballot = __ballot_sync(0xffffffffu, hit);
+  const int k = valid ? edge_point(A.n_interp, o) : 0x7fffffff;
+  const int kmin = __reduce_min_sync(0xffffffffu, hit ? k : 0x7fffffff);
+  if (!in_range || lane != 0) return;
+  const int32_t e = A.active ? A.active[slot] : (int32_t)slot;
+  if (ballot) {
+    A.in_collision[e] = 1;
+    if (A.hit_index) A.hit_index[e] = kmin;
+  } else if ((A.round + 1) * 32 >= A.n_interp) {
+    A.in_collision[e] = 0;
+    if (A.hit_index) A.hit_index[e] = -1;
+  } else {
+    A.next_active[atomicAdd(A.next_count, 1)] = e;
+  }
+}
+
+template <int MP, int KIND, int MODE>
+__global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ ScoreArgs A,
+                                                    const __grid_constant__ FkParams P) {
+  constexpr int QT = qt_for(MP);
+  constexpr int NP = MP / 2;
+  constexpr int64_t TF = tile_floats(MP);
+  constexpr uint32_t TB = (uint32_t)tile_bytes(MP);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  float* stages = reinterpret_cast<float*>(smem_raw + 128);
+
+  const int tid = threadIdx.x;
+  const int64_t qb = blockIdx.x / A.n_splits;
+  const int split = blockIdx.x % A.n_splits;
+  const int64_t q_base = qb * (int64_t)(kNT * QT);
+  const int64_t nq_live = MODE == MODE_EDGE ? edge_active_queries(A) : A.nq;
+  if (q_base >= nq_live) return;  // uniform: whole CTA idle (edge rounds sized for the worst case)
+
+  const int64_t t0 = (int64_t)split * A.tiles_per_split;
+  const int64_t t1 = min(t0 + (int64_t)A.tiles_per_split, A.n_tiles);
+  const int nt = (int)max(t1 - t0, (int64_t)0);
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < kStages && s < nt; ++s) {
+      mbar_expect_tx(&bars[s], TB);
+      tma_bulk_g2s(stages + s * TF, A.packed + (t0 + s) * TF, TB, &bars[s]);
+    }
+  }
+
+  // ---- queries -> scaled control points in registers (f32x2 pairs over m) ----
+  f2 ux[QT][NP], uy[QT][NP], uz[QT][NP];
+#pragma unroll
+  for (int j = 0; j < QT; ++j) {
+    const int64_t vq = q_base + j * kNT + tid;
+    float px[MP], py[MP], pz[MP];
+#pragma unroll
+    for (int m = 0; m < MP; ++m) px[m] = py[m] = pz[m] = 0.0f;
+    if (MODE == MODE_POS) {
+      if (vq < A.nq) {
+#pragma unroll
+        for (int m = 0; m < MP; ++m) {
+          if (m < A.M) {
+            const float4 v = __ldg(A.qpos + (int64_t)m * A.ldq + vq);
+            px[m] = v.x; py[m] = v.y; pz[m] = v.z;
+          }
+        }
+      }
+    } else {
+      const int64_t slot = vq >> 5;
+      const int o = A.round * 32 + (int)(vq & 31);
+      if (vq < nq_live && o < A.n_interp) {
+        const int32_t e = A.active ? A.active[slot] : (int32_t)slot;
+        const int k = edge_point(A.n_interp, o);
+        const float t = A.n_interp > 1 ? __fdiv_rn((float)k, (float)(A.n_interp - 1)) : 0.0f;
+        const float* qa = A.qa + (int64_t)e * A.ldqe;
+        const float* qb2 = A.qb + (int64_t)e * A.ldqe;
+        float tmp[MP][3];
+        fk_chain(
+            P,
+            [&](int jj) {
+              const float a = __ldg(qa + jj), b = __ldg(qb2 + jj);
+              return (double)__fadd_rn(a, __fmul_rn(t, __fsub_rn(b, a)));
+            },
+            [&](int m, double x, double y, double z) {
+              tmp[m][0] = __double2float_rn(x);
+              tmp[m][1] = __double2float_rn(y);
+              tmp[m][2] = __double2float_rn(z);
+            });
+#pragma unroll
+        for (int m = 0; m < MP; ++m)
+          if (m < A.M) { px[m] = tmp[m][0]; py[m] = tmp[m][1]; pz[m] = tmp[m][2]; }
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      ux[j][p] = pk(__fmul_rn(px[2 * p], A.scale), __fmul_rn(px[2 * p + 1], A.scale));
+      uy[j][p] = pk(__fmul_rn(py[2 * p], A.scale), __fmul_rn(py[2 * p + 1], A.scale));
+      uz[j][p] = pk(__fmul_rn(pz[2 * p], A.scale), __fmul_rn(pz[2 * p + 1], A.scale));
+    }
+  }
+
+  double f[QT];
+#pragma unroll
+  for (int j = 0; j < QT; ++j) f[j] = 0.0;
+
+  // ---- stream the support tiles ----
+  for (int it = 0; it < nt; ++it) {
+    const int st = it % kStages;
+    mbar_wait(&bars[st], (uint32_t)((it / kStages) & 1));
+    const float* T = stages + st * TF;
+    const float* alpha = T + kTileSupports * NP * 8;
+#pragma unroll 1
+    for (int g = 0; g < kTileSupports; g += kGroup) {
+      float part[QT];
+#pragma unroll
+      for (int j = 0; j < QT; ++j) part[j] = 0.0f;
+#pragma unroll 2
+      for (int u = 0; u < kGroup; ++u) {
+        const float* rec = T + (g + u) * NP * 8;
+        f2 acc[QT];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          const float4 xy = *reinterpret_cast<const float4*>(rec + p * 8);
+          const float2 zz = *reinterpret_cast<const float2*>(rec + p * 8 + 4);
+          const f2 vx = pk(xy.x, xy.y), vy = pk(xy.z, xy.w), vz = pk(zz.x, zz.y);
+#pragma unroll
+          for (int j = 0; j < QT; ++j) {
+            const f2 t = term_pair<KIND>(ux[j][p], uy[j][p], uz[j][p], vx, vy, vz);
+            acc[j] = p == 0 ? t : add2(acc[j], t);
+          }
+        }
+        const float a = alpha[g + u];
+#pragma unroll
+        for (int j = 0; j < QT; ++j) part[j] = __fmaf_rn(a, pair_sum(acc[j]), part[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < QT; ++j) f[j] += (double)part[j];
+    }
+    __syncthreads();  // every thread is done with stage st
+    if (tid == 0 && it + kStages < nt) {
+      fence_proxy_async();
+      mbar_expect_tx(&bars[st], TB);
+      tma_bulk_g2s(stages + st * TF, A.packed + (t0 + it + kStages) * TF, TB, &bars[st]);
+    }
+  }
+
+  // ---- epilogue ----
+#pragma unroll
+  for (int j = 0; j < QT; ++j) {
+    const int64_t vq = q_base + j * kNT + tid;
+    if (A.n_splits > 1) {
+      if (vq < nq_live) A.partial[(int64_t)split * A.nq + vq] = f[j];
+    } else if (MODE == MODE_POS) {
+      if (vq < A.nq) {
+        const double fm = f[j] / (double)A.M;
+        if (A.score) A.score[vq] = (float)fm;
+        if (A.label) A.label[vq] = fm > 0.0 ? 1 : -1;
+      }
+    } else {
+      edge_vote(A, vq, f[j] / (double)A.M);
+    }
+  }
+}
+
+// Fixed-order reduction of the split partials (deterministic), then 1/M, score, label / vote.
+template <int MODE>
+__global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ ScoreArgs A) {
+  const int64_t vq = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nq_live = MODE == MODE_EDGE ? edge_active_queries(A) : A.nq;
+  if (MODE == MODE_EDGE) {
+    if ((vq & ~(int64_t)31) >= nq_live) return;  // warp-uniform
+  } else if (vq >= A.nq) {
+    return;
+  }
+  double f = 0.0;
+  if (vq < nq_live)
+    for (int s = 0; s < A.n_splits; ++s) f += A.partial[(int64_t)s * A.nq + vq];
+  const double fm = f / (double)A.M;
+  if (MODE == MODE_POS) {
+    if (A.score) A.score[vq] = (float)fm;
+    if (A.label) A.label[vq] = fm > 0.0 ? 1 : -1;
+  } else {
+    edge_vote(A, vq, fm);
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// planning + dispatch
+// ---------------------------------------------------------------------------------
+int score_max_splits(int64_t nq, int64_t ns, int M) {
+  const int64_t qblocks = (nq + score_queries_per_cta(M) - 1) / score_queries_per_cta(M);
+  const int64_t tiles = n_support_tiles(ns);
+  if (qblocks <= 0 || tiles <= 1) return 1;
+  // enough units for ~8 waves of 148 SMs x 4 CTAs; never more splits than tiles
+  int64_t cap = (8 * 148 * 4 + qblocks - 1) / qblocks;
+  cap = cap < 1 ? 1 : cap;
+  cap = cap > 64 ? 64 : cap;
+  return (int)(cap < tiles ? cap : tiles);
+}
+
+size_t score_partial_bytes(int64_t nq, int64_t ns, int M) {
+  const int s = score_max_splits(nq, ns, M);
+  return s > 1 ? (size_t)s * (size_t)nq * sizeof(double) : 0;
+}
+
+template <int MP, int KIND, int MODE>
+static int score_ctas_per_sm() {
+  static int cached = -1;
+  if (cached < 0) {
+    const size_t smem = 128 + kStages * tile_bytes(MP);
+    int n = 0;
+    cudaFuncSetAttribute(score_kernel<MP, KIND, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, score_kernel<MP, KIND, MODE>, kNT, smem);
+    cached = n > 0 ? n : 1;
+  }
+  return cached;
+}
+
+static ScorePlan make_plan(int64_t nq, int64_t ns, int M, int ctas_per_sm) {
+  ScorePlan p;
+  const int qpc = score_queries_per_cta(M);
+  p.n_qblocks = (nq + qpc - 1) / qpc;
+  p.n_tiles = n_support_tiles(ns);
+  const int64_t slots = (int64_t)device_info().sms * ctas_per_sm;
+  const int max_s = score_max_splits(nq, ns, M);
+  int best = 1;
+  double best_score = -1.0;
+  for (int s = 1; s <= max_s; ++s) {
+    const int64_t tps = (p.n_tiles + s - 1) / s;
+    const int64_t s_eff = tps > 0 ? (p.n_tiles + tps - 1) / tps : 1;  // splits actually non-empty
+    if (s_eff != s) continue;
+    const int64_t units = p.n_qblocks * s;
+    const int64_t waves = (units + slots - 1) / slots;
+    const double eff = (double)units / (double)(waves * slots);
+    const double sc = eff - 0.004 * s;  // mild preference for fewer splits (partials + finalize)
+    if (sc > best_score + 1e-12) { best_score = sc; best = s; }
+  }
+  p.n_splits = best;
+  p.tiles_per_split = (int32_t)(p.n_tiles > 0 ? (p.n_tiles + best - 1) / best : 0);
+  return p;
+}
+
+template <int MP, int KIND, int MODE>
+static cudaError_t run_score(const ScoreArgs& base, const FkParams& P, int64_t nq, int64_t ns, cudaStream_t st) {
+  const ScorePlan plan = make_plan(nq, ns, base.M, score_ctas_per_sm<MP, KIND, MODE>());
+  ScoreArgs A = base;
+  A.n_tiles = plan.n_tiles;
+  A.n_splits = plan.n_splits;
+  A.tiles_per_split = plan.tiles_per_split;
+  const size_t smem = 128 + kStages * tile_bytes(MP);
+  const int64_t grid = plan.n_qblocks * plan.n_splits;
+  if (grid > 0x7fffffff) return cudaErrorInvalidValue;
+  score_kernel<MP, KIND, MODE><<<(unsigned)grid, kNT, smem, st>>>(A, P);
+  g_launches.fetch_add(1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || plan.n_splits == 1) return e;
+  const int64_t fgrid = (nq + 255) / 256;
+  finalize_kernel<MODE><<<(unsigned)fgrid, 256, 0, st>>>(A);
+  g_launches.fetch_add(1);
+  return cudaGetLastError();
+}
+
+template <int MODE>
+static cudaError_t dispatch(const ScoreArgs& A, const FkParams& P, int64_t nq, int64_t ns, int kind, cudaStream_t st) {
+  const int MP = padded_m(A.M);
+#define FASTRON_CASE(mp)                                                                   \
+  case mp:                                                                                 \
+    return kind == kGaussian ? run_score<mp, kGaussian, MODE>(A, P, nq, ns, st)            \
+                             : run_score<mp, kRQ, MODE>(A, P, nq, ns, st);
+  switch (MP) {
+    FASTRON_CASE(2)
+    FASTRON_CASE(4)
+    FASTRON_CASE(6)
+    FASTRON_CASE(8)
+    FASTRON_CASE(10)
+    FASTRON_CASE(12)
+    FASTRON_CASE(14)
+    FASTRON_CASE(16)
+    FASTRON_CASE(18)
+    FASTRON_CASE(20)
+    FASTRON_CASE(22)
+    FASTRON_CASE(24)
+    FASTRON_CASE(26)
+    FASTRON_CASE(28)
+    FASTRON_CASE(30)
+    FASTRON_CASE(32)
+    default:
+      return cudaErrorInvalidValue;
+  }
+#undef FASTRON_CASE
+}
+
+ScorePlan plan_score(int64_t nq, int64_t ns, int M, int kind) {
+  (void)kind;
+  return make_plan(nq, ns, M, 3);
+}
+
+cudaError_t launch_score(const float4* qpos, int64_t nq, int64_t ldq, const float* packed, int64_t ns, int M, int kind,
+                         float scale, float* score, int8_t* label, double* partial, cudaStream_t st) {
+  if (nq <= 0) return cudaSuccess;
+  ScoreArgs A = {};
+  A.qpos = qpos;
+  A.ldq = ldq;
+  A.nq = nq;
+  A.packed = packed;
+  A.M = M;
+  A.scale = scale;
+  A.score = score;
+  A.label = label;
+  A.partial = partial;
+  FkParams P = {};
+  return dispatch<MODE_POS>(A, P, nq, ns, kind, st);
+}
+
+cudaError_t launch_edge_round(const FkParams& P, const EdgeRound& R, const float* packed, int64_t ns, int M, int kind,
+                              float scale, double* partial, cudaStream_t st) {
+  if (R.n_edges <= 0) return cudaSuccess;
+  ScoreArgs A = {};
+  A.nq = R.n_edges * 32;
+  A.packed = packed;
+  A.M = M;
+  A.scale = scale;
+  A.partial = partial;
+  A.qa = R.qa;
+  A.qb = R.qb;
+  A.ldqe = R.ldq;
+  A.n_interp = R.n_interp;
+  A.round = R.round;
+  A.active = R.active;
+  A.active_count = R.active_count;
+  A.next_active = R.next_active;
+  A.next_count = R.next_count;
+  A.in_collision = R.in_collision;
+  A.hit_index = R.hit_index;
+  return dispatch<MODE_EDGE>(A, P, A.nq, ns, kind, st);
+}
+
+}  // namespace fastron

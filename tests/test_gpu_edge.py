@@ -1,0 +1,100 @@
+"""GPU parity of fastron_edge_check (K4: interpolate -> FK -> score -> warp vote) against
+the oracle edge check (BASELINE.json cfg4; R11)."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from gpu_helpers import dev, require_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu_edges(robot, qa, qb, n_interp, sup, alpha, kind, gamma):
+    import torch
+    import paper_1910_06451_b200 as fb
+    spos = fb.fastron_fk(robot, dev(sup))
+    hit, idx = fb.fastron_edge_check(robot, dev(qa), dev(qb), n_interp, spos, dev(alpha), kind, gamma)
+    torch.cuda.synchronize()
+    return hit.cpu().numpy(), idx.cpu().numpy()
+
+
+def _order(n):
+    return [2 * o for o in range((n + 1) // 2)] + [2 * o + 1 for o in range(n // 2)]
+
+
+def _check(robot, qa, qb, n_interp, sup, alpha, kind, gamma):
+    hit, idx = _gpu_edges(robot, qa, qb, n_interp, sup, alpha, kind, gamma)
+    ref_hit, fmax, fall = oracle.edge(robot, qa, qb, n_interp, kind, gamma, oracle.fk(robot, sup), alpha,
+                                      with_all=True)
+    sure = np.abs(fmax) > 1e-4
+    bad = np.flatnonzero(sure & (hit != ref_hit))
+    assert bad.size == 0, f"{bad.size} edge label mismatches, e.g. {bad[:5]} fmax {fmax[bad[:5]]}"
+    order = _order(n_interp)
+    for e in range(len(hit)):
+        if hit[e]:
+            k = idx[e]
+            assert 0 <= k < n_interp and fall[e, k] > -1e-4
+            r = order.index(k) // 32  # the round that reported the hit; earlier rounds had no hit
+            earlier = [order[o] for o in range(0, 32 * r)]
+            assert np.all(fall[e, earlier] <= 1e-4)
+            same_round = [order[o] for o in range(32 * r, min(32 * r + 32, n_interp))]
+            pos_in_round = [kk for kk in same_round if fall[e, kk] > 1e-4]
+            if pos_in_round:
+                assert k <= min(pos_in_round)
+        else:
+            assert idx[e] == -1
+    return hit, ref_hit, fmax
+
+
+def test_cfg4_subset():
+    require_gpu()
+    wl = W.edge_workload(n_edges=1500)
+    hit, ref, fmax = _check(wl.robot, wl.qa, wl.qb, wl.n_interp, wl.supports, wl.alpha, 0, wl.gamma)
+    assert 0 < hit.sum() < len(hit)
+
+
+@pytest.mark.parametrize("n_interp", [1, 2, 33, 64, 100])
+def test_interp_counts_and_rounds(n_interp):
+    require_gpu()
+    wl = W.edge_workload(n_edges=300, n_supports=700)
+    # shorter edges so that both outcomes are frequent
+    qb = (wl.qa + 0.25 * (wl.qb - wl.qa)).astype(np.float32)
+    _check(wl.robot, wl.qa, qb, n_interp, wl.supports, wl.alpha, 1, wl.gamma)
+
+
+def test_degenerate_and_endpoint_edges():
+    """a = b free -> 0; an endpoint with f > 0 -> 1."""
+    require_gpu()
+    wl = W.edge_workload(n_edges=10, n_supports=500)
+    q = np.random.default_rng(0).uniform(-np.pi, np.pi, size=(3000, 7)).astype(np.float32)
+    f, _ = oracle.score(0, wl.gamma, oracle.fk(wl.robot, q), oracle.fk(wl.robot, wl.supports), wl.alpha)
+    nb = min(int(np.sum(f < -1e-3)), int(np.sum(f > 1e-3)), 50)
+    assert nb >= 8
+    free = q[f < -1e-3][:nb]
+    bad = q[f > 1e-3][:nb]
+    hit, idx = _gpu_edges(wl.robot, free, free, 64, wl.supports, wl.alpha, 0, wl.gamma)
+    assert np.all(hit == 0) and np.all(idx == -1)
+    hit, idx = _gpu_edges(wl.robot, bad, free, 64, wl.supports, wl.alpha, 0, wl.gamma)
+    assert np.all(hit == 1) and np.all(idx == 0)  # k = 0 is the first point of round 1
+    hit, idx = _gpu_edges(wl.robot, free, bad, 64, wl.supports, wl.alpha, 0, wl.gamma)
+    assert np.all(hit == 1)
+
+
+def test_edge_equals_or_of_scores():
+    """T2: in_collision == OR_k (fastron_score(fastron_fk(q_k)) > 0) with q_k interpolated in
+    fp32 exactly as the kernel does (t = k/(n-1), q = a + t (b - a), each op rounded)."""
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    wl = W.edge_workload(n_edges=400, n_supports=900)
+    hit, _ = _gpu_edges(wl.robot, wl.qa, wl.qb, 64, wl.supports, wl.alpha, 0, wl.gamma)
+    t = (np.arange(64, dtype=np.float32) / np.float32(63)).astype(np.float32)
+    d = (wl.qb - wl.qa).astype(np.float32)
+    pts = (wl.qa[:, None, :] + (t[None, :, None] * d[:, None, :]).astype(np.float32)).astype(np.float32)
+    spos = fb.fastron_fk(wl.robot, dev(wl.supports))
+    qpos = fb.fastron_fk(wl.robot, dev(pts.reshape(-1, 7)))
+    _, lab = fb.fastron_score(qpos, spos, dev(wl.alpha), 0, wl.gamma)
+    torch.cuda.synchronize()
+    any_pos = (lab.cpu().numpy().reshape(400, 64) > 0).any(axis=1)
+    assert np.array_equal(hit.astype(bool), any_pos)

@@ -1,0 +1,143 @@
+"""GPU parity of fastron_gram (K3) and fastron_train (K5, Algorithm 1) against the
+oracle, plus the cross-kernel identity Gram == score(alpha = e_i)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from gpu_helpers import assert_score_parity, dev, positions_np, require_gpu
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gram(robot, X, kind, gamma):
+    import torch
+    import paper_1910_06451_b200 as fb
+    pos = fb.fastron_fk(robot, dev(X))
+    K = fb.fastron_gram(pos, kind, gamma)
+    torch.cuda.synchronize()
+    return pos, K
+
+
+@pytest.mark.parametrize("n,kind", [(1, 0), (127, 0), (300, 1), (1000, 0), (1000, 1)])
+def test_gram_parity_symmetry_diagonal(n, kind):
+    require_gpu()
+    wl = W.train_workload(n)
+    _, K = _gram(wl.robot, wl.X, kind, wl.gamma)
+    Kg = K.cpu().numpy()
+    assert np.array_equal(Kg, Kg.T)  # mirrored tiles: exactly symmetric
+    assert np.all(np.diag(Kg) == 1.0)  # R18: d^2 = 0 -> every term exactly 1
+    Kr = oracle.gram(kind, wl.gamma, oracle.fk(wl.robot, wl.X))
+    assert_score_parity(Kg.ravel(), Kr.ravel(), what=f"gram n={n}")
+    if n <= 300 and n > 1:
+        ev = np.linalg.eigvalsh(Kg.astype(np.float64))
+        assert ev[0] >= -1e-6 * ev[-1]  # Claim 1 up to fp32 rounding
+
+
+def test_gram_m16_and_ldk():
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    robot, X, _, _ = W.cfg5_gram_workload(400)
+    pos = fb.fastron_fk(robot, dev(X))
+    K = torch.full((400, 416), -3.0, device="cuda")
+    fb.fastron_gram(pos, 0, 5.0, K=K[:, :400])  # ldk = 416
+    torch.cuda.synchronize()
+    Kh = K.cpu().numpy()
+    assert np.all(Kh[:, 400:] == -3.0)
+    Kr = oracle.gram(0, 5.0, oracle.fk(robot, X))
+    assert_score_parity(Kh[:, :400].ravel(), Kr.ravel(), what="gram M=16")
+
+
+def test_gram_equals_score_with_unit_alpha():
+    """T2 cross-kernel identity: K[i, j] == fastron_score(x_j; supports X, alpha = e_i) bit for bit."""
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    wl = W.train_workload(260)
+    pos, K = _gram(wl.robot, wl.X, 0, wl.gamma)
+    Kh = K.cpu().numpy()
+    for i in (0, 1, 63, 64, 200, 259):
+        alpha = torch.zeros(260, device="cuda")
+        alpha[i] = 1.0
+        s, _ = fb.fastron_score(pos, pos, alpha, 0, wl.gamma)
+        torch.cuda.synchronize()
+        assert np.array_equal(s.cpu().numpy(), Kh[i]), i
+
+
+def _labels(wl):
+    pos = oracle.fk(wl.robot, wl.X)
+    return W.capsule_aabb_labels(W.chain_points(pos), wl.cubes, wl.radius)
+
+
+def _gpu_train(K, y, beta, iter_max, s_max=None, alpha0=None, F0=None):
+    import torch
+    import paper_1910_06451_b200 as fb
+    out = fb.fastron_train(K, dev(y), beta, iter_max, s_max,
+                           alpha=None if alpha0 is None else dev(alpha0, torch.float64),
+                           F=None if F0 is None else dev(F0, torch.float64))
+    torch.cuda.synchronize()
+    res = fb.train_result(out["result"])
+    return dict(alpha=out["alpha"].cpu().numpy(), F=out["F"].cpu().numpy(),
+                trace=out["trace"].cpu().numpy()[:res["iterations"]],
+                support=out["support_idx"].cpu().numpy()[:res["n_support"]], **res)
+
+
+def _assert_same_run(g, r):
+    assert g["iterations"] == r["iterations"] and g["n_add"] == r["n_add"] and g["n_remove"] == r["n_remove"]
+    assert np.array_equal(g["trace"], r["trace"]), np.flatnonzero(g["trace"] != r["trace"])[:5]
+    assert g["converged"] == r["converged"] and g["n_support"] == r["n_support"]
+    assert np.array_equal(g["support"], r["support"])
+    scale = max(1.0, float(np.abs(r["alpha"]).max()))
+    assert np.abs(g["alpha"] - r["alpha"]).max() <= 1e-9 * scale
+    assert np.abs(g["F"] - r["F"]).max() <= 1e-9 * max(1.0, float(np.abs(r["F"]).max()))
+
+
+@pytest.mark.parametrize("n,beta,s_max", [(1000, 1.0, None), (1000, 2.0, None), (1000, 1.0, 50), (5000, 1.0, None)])
+def test_train_trace_exact_on_gpu_gram(n, beta, s_max):
+    """P-exact mode: the oracle's Algorithm 1 on the GPU's fp32 Gram
+    promoted to fp64 must give the identical trace and alpha. n = 5000 is cfg3 itself."""
+    require_gpu()
+    wl = W.train_workload(n)
+    y = _labels(wl)
+    _, K = _gram(wl.robot, wl.X, 0, wl.gamma)
+    g = _gpu_train(K, y, beta, wl.iter_max, s_max)
+    r = oracle.train(K.cpu().numpy().astype(np.float64), y, beta, wl.iter_max, s_max)
+    _assert_same_run(g, r)
+
+
+def test_train_warm_start_and_iter_max():
+    require_gpu()
+    wl = W.train_workload(800)
+    y = _labels(wl)
+    _, K = _gram(wl.robot, wl.X, 1, wl.gamma)
+    K64 = K.cpu().numpy().astype(np.float64)
+    first = oracle.train(K64, y, 1.0, 300)
+    y2 = y.copy()
+    y2[::7] *= -1  # labels move: retrain from the previous model
+    g = _gpu_train(K, y2, 1.0, 20000, alpha0=first["alpha"], F0=first["F"])
+    r = oracle.train(K64, y2, 1.0, 20000, alpha0=first["alpha"], F0=first["F"])
+    _assert_same_run(g, r)
+    g0 = _gpu_train(K, y2, 1.0, 0)
+    assert g0["iterations"] == 0 and not g0["converged"]
+
+
+@pytest.mark.parametrize("case", json.load(open(os.path.join(GOLD, "train_cases.json")))["cases"],
+                         ids=lambda c: c["name"])
+def test_train_hand_derived_cases(case):
+    require_gpu()
+    import torch
+    K = torch.tensor(case["K"], dtype=torch.float32, device="cuda")
+    K64 = K.cpu().numpy().astype(np.float64)  # 0.9 is not an fp32 value: compare to the fp32-K oracle run
+    y = np.array(case["y"], dtype=np.int8)
+    g = _gpu_train(K, y, case["beta"], case["iter_max"], case["s_max"], case.get("alpha0"),
+                   None if "F0" not in case else (K64 @ np.array(case["alpha0"])))
+    r = oracle.train(K64, y, case["beta"], case["iter_max"], case["s_max"], alpha0=case.get("alpha0"),
+                     F0=None if "F0" not in case else (K64 @ np.array(case["alpha0"])))
+    _assert_same_run(g, r)
+    np.testing.assert_allclose(g["alpha"], case["alpha"], atol=1e-6)
+    assert g["trace"].tolist() == case["trace"]

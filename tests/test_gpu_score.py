@@ -1,0 +1,166 @@
+"""GPU parity of fastron_score (K2) against the oracle score (PAPER.md:183 with Eq. 4),
+end to end from fp32 joint configurations: GPU = fastron_fk + fastron_score, oracle =
+fp64 FK + fp64 kernel sums. Tolerance: BASELINE.json north_star (R16)."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from gpu_helpers import assert_score_parity, dev, require_gpu, soa_from_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu_scores(robot, supports, alpha, queries, kind, gamma):
+    import torch
+    import paper_1910_06451_b200 as fb
+    spos = fb.fastron_fk(robot, dev(supports))
+    qpos = fb.fastron_fk(robot, dev(queries))
+    s, l = fb.fastron_score(qpos, spos, dev(alpha), kind, gamma)
+    torch.cuda.synchronize()
+    return s.cpu().numpy(), l.cpu().numpy()
+
+
+def _ref_scores(robot, supports, alpha, queries, kind, gamma):
+    return oracle.score(kind, gamma, oracle.fk(robot, queries), oracle.fk(robot, supports), alpha)
+
+
+@pytest.mark.parametrize("kind", [W.GAUSSIAN, W.RQ])
+def test_cfg1_full(kind):
+    require_gpu()
+    wl = W.score_workload("cfg1", kind=kind)
+    s, l = _gpu_scores(wl.robot, wl.supports, wl.alpha, wl.queries, kind, wl.gamma)
+    f, _ = _ref_scores(wl.robot, wl.supports, wl.alpha, wl.queries, kind, wl.gamma)
+    assert_score_parity(s, f, l, what=f"cfg1 kind={kind}")
+
+
+@pytest.mark.parametrize("kind", [W.GAUSSIAN, W.RQ])
+def test_cfg2_subset(kind):
+    """cfg2 supports (2,000) against the first 100,003 queries: many tiles + ragged tails."""
+    require_gpu()
+    wl = W.score_workload("cfg2", n_queries=100_003, kind=kind)
+    s, l = _gpu_scores(wl.robot, wl.supports, wl.alpha, wl.queries, kind, wl.gamma)
+    f, _ = _ref_scores(wl.robot, wl.supports, wl.alpha, wl.queries, kind, wl.gamma)
+    assert_score_parity(s, f, l, what=f"cfg2 kind={kind}")
+
+
+def test_cfg5_subset_m16():
+    require_gpu()
+    wl = W.score_workload("cfg5", n_queries=20_000, n_supports=5_000)
+    s, l = _gpu_scores(wl.robot, wl.supports, wl.alpha, wl.queries, 0, wl.gamma)
+    f, _ = _ref_scores(wl.robot, wl.supports, wl.alpha, wl.queries, 0, wl.gamma)
+    assert_score_parity(s, f, l, what="cfg5 M=16")
+
+
+def test_headline_full_size_sampled():
+    """Headline size (1M queries x 20k supports, the bench launch configuration):
+    the oracle recomputes a seeded sample of 1,000 queries plus the 500 GPU scores
+    nearest zero (the label boundary)."""
+    require_gpu()
+    wl = W.score_workload("headline")
+    s, l = _gpu_scores(wl.robot, wl.supports, wl.alpha, wl.queries, 0, wl.gamma)
+    rng = np.random.default_rng(0)
+    idx = np.unique(np.concatenate([rng.choice(len(s), 1000, replace=False), np.argsort(np.abs(s))[:500]]))
+    f, _ = _ref_scores(wl.robot, wl.supports, wl.alpha, wl.queries[idx], 0, wl.gamma)
+    assert_score_parity(s[idx], f, l[idx], what="headline sample")
+
+
+@pytest.mark.parametrize("M", [1, 3, 5, 32])
+def test_odd_and_extreme_m(M):
+    """Padded control points (odd M) contribute exactly 0; M = 32 is the maximum."""
+    require_gpu()
+    base = W.arm7(8)
+    rng = np.random.default_rng(M)
+    frames = rng.integers(0, 8, size=M)
+    offs = rng.uniform(-0.1, 0.1, size=(M, 3))
+    robot = W.make_robot("m%d" % M, base.dh, frames, offs)
+    sup = rng.uniform(-np.pi, np.pi, size=(333, 7)).astype(np.float32)
+    alpha = rng.standard_normal(333).astype(np.float32)
+    q = rng.uniform(-np.pi, np.pi, size=(1500, 7)).astype(np.float32)
+    for kind in (0, 1):
+        s, l = _gpu_scores(robot, sup, alpha, q, kind, 5.0)
+        f, _ = _ref_scores(robot, sup, alpha, q, kind, 5.0)
+        assert_score_parity(s, f, l, what=f"M={M} kind={kind}")
+
+
+@pytest.mark.parametrize("ns,nq", [(0, 100), (1, 1), (1, 700), (65, 3), (64, 513), (129, 10_000)])
+def test_edge_sizes(ns, nq):
+    require_gpu()
+    robot = W.arm7(8)
+    rng = np.random.default_rng(ns * 7 + nq)
+    sup = rng.uniform(-np.pi, np.pi, size=(ns, 7)).astype(np.float32)
+    alpha = rng.standard_normal(ns).astype(np.float32)
+    q = rng.uniform(-np.pi, np.pi, size=(nq, 7)).astype(np.float32)
+    if ns == 0:
+        import torch
+        import paper_1910_06451_b200 as fb
+        qpos = fb.fastron_fk(robot, dev(q))
+        spos = torch.empty((8, 0, 4), device="cuda")
+        s, l = fb.fastron_score(qpos, spos, torch.empty(0, device="cuda"), 0, 5.0)
+        assert np.all(s.cpu().numpy() == 0) and np.all(l.cpu().numpy() == -1)
+        return
+    s, l = _gpu_scores(robot, sup, alpha, q, 0, 5.0)
+    f, _ = _ref_scores(robot, sup, alpha, q, 0, 5.0)
+    assert_score_parity(s, f, l, what=f"ns={ns} nq={nq}")
+
+
+def test_self_support_gives_exactly_one():
+    """One support at the query with alpha = 1 -> f = k(q, q) = 1 exactly (R18)."""
+    require_gpu()
+    robot = W.arm7(8)
+    q = np.random.default_rng(1).uniform(-np.pi, np.pi, size=(50, 7)).astype(np.float32)
+    for kind in (0, 1):
+        for i in range(0, 50, 7):
+            s, l = _gpu_scores(robot, q[i:i + 1], np.ones(1, np.float32), q[i:i + 1], kind, 5.0)
+            assert s[0] == 1.0 and l[0] == 1
+
+
+def test_deterministic_and_positions_input():
+    """Bit-reproducible across runs; and fastron_score on oracle-rounded positions matches the
+    oracle score of those same fp32 positions (the score stage alone)."""
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    wl = W.score_workload("cfg2", n_queries=5000, n_supports=700)
+    s1, l1 = _gpu_scores(wl.robot, wl.supports, wl.alpha, wl.queries, 0, wl.gamma)
+    s2, l2 = _gpu_scores(wl.robot, wl.supports, wl.alpha, wl.queries, 0, wl.gamma)
+    assert np.array_equal(s1, s2) and np.array_equal(l1, l2)
+    qp = oracle.fk(wl.robot, wl.queries).astype(np.float32).astype(np.float64)
+    sp = oracle.fk(wl.robot, wl.supports).astype(np.float32).astype(np.float64)
+    s, l = fb.fastron_score(soa_from_oracle(qp), soa_from_oracle(sp), dev(wl.alpha), 0, wl.gamma)
+    torch.cuda.synchronize()
+    f, _ = oracle.score(0, wl.gamma, qp, sp, wl.alpha)
+    assert_score_parity(s.cpu().numpy(), f, l.cpu().numpy(), what="positions input")
+
+
+def test_linearity_in_alpha():
+    require_gpu()
+    wl = W.score_workload("cfg1", n_queries=3000, n_supports=300)
+    s1, _ = _gpu_scores(wl.robot, wl.supports, wl.alpha, wl.queries, 0, wl.gamma)
+    s2, _ = _gpu_scores(wl.robot, wl.supports, (2 * wl.alpha).astype(np.float32), wl.queries, 0, wl.gamma)
+    assert np.array_equal(s2, 2 * s1)  # scaling alpha by 2 is exact in binary floating point
+
+
+def test_query_host_pipeline_matches_device_path():
+    """fastron_query with pinned host buffers (chunked H2D/D2H overlap) equals fk + score."""
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    wl = W.score_workload("cfg2", n_queries=600_000, n_supports=500)
+    spos = fb.fastron_fk(wl.robot, dev(wl.supports))
+    alpha = dev(wl.alpha)
+    s_dev, l_dev = _gpu_scores(wl.robot, wl.supports, wl.alpha, wl.queries, 0, wl.gamma)
+    qh = torch.from_numpy(wl.queries).pin_memory()
+    sh = torch.empty(len(wl.queries), dtype=torch.float32).pin_memory()
+    lh = torch.empty(len(wl.queries), dtype=torch.int8).pin_memory()
+    fb.fastron_query(wl.robot, qh, spos, alpha, 0, wl.gamma, score=sh, label=lh)
+    assert np.array_equal(sh.numpy(), s_dev) and np.array_equal(lh.numpy(), l_dev)
+    # pageable host memory and device tensors work too
+    qp = torch.from_numpy(wl.queries[:1000].copy())
+    sp = torch.empty(1000, dtype=torch.float32)
+    fb.fastron_query(wl.robot, qp, spos, alpha, 0, wl.gamma, score=sp)
+    assert np.array_equal(sp.numpy(), s_dev[:1000])
+    sd = torch.empty(1000, dtype=torch.float32, device="cuda")
+    fb.fastron_query(wl.robot, dev(wl.queries[:1000]), spos, alpha, 0, wl.gamma, score=sd)
+    torch.cuda.synchronize()
+    assert np.array_equal(sd.cpu().numpy(), s_dev[:1000])
