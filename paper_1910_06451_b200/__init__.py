@@ -17,7 +17,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfastron_b200.so")
+LIB_PATH = os.environ.get("FASTRON_LIB", os.path.join(_HERE, "libfastron_b200.so"))
 
 FASTRON_OK, FASTRON_ERR_INVALID_ARG, FASTRON_ERR_CUDA, FASTRON_ERR_WORKSPACE, FASTRON_ERR_UNSUPPORTED = range(5)
 GAUSSIAN, RQ = 0, 1

@@ -23,13 +23,14 @@ constexpr int kRQ = 1;
 
 // Support tile: TS supports per tile. Each support is MP/2 pair records of 8 floats
 // (x_m, x_m+1, y_m, y_m+1, z_m, z_m+1, 0, 0), pre-scaled, followed after the TS
-// records by TS alpha values. Padded control points (m >= M) hold kPadCoord so their
-// term is exactly 0; padded supports (index >= ns) hold zeros and alpha = 0.
+// records by TS alpha values stored as double (the fp64 accumulation operand).
+// Padded control points (m >= M) hold kPadCoord so their term is exactly 0; padded
+// supports (index >= ns) hold zeros and alpha = 0.
 constexpr int kTileSupports = 64;
 constexpr float kPadCoord = 1.0e30f;
 
-__host__ __device__ constexpr int pair_floats() { return 8; }
-__host__ __device__ constexpr int64_t tile_floats(int mp) { return (int64_t)kTileSupports * (mp / 2) * 8 + kTileSupports; }
+__host__ __device__ constexpr int64_t tile_record_floats(int mp) { return (int64_t)kTileSupports * (mp / 2) * 8; }
+__host__ __device__ constexpr int64_t tile_floats(int mp) { return tile_record_floats(mp) + 2 * kTileSupports; }
 __host__ __device__ constexpr int64_t tile_bytes(int mp) { return tile_floats(mp) * 4; }
 
 // ---------------------------------------------------------------------------------
@@ -42,18 +43,8 @@ __device__ __forceinline__ f2 pk(float lo, float hi) {
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
   return r;
 }
-__device__ __forceinline__ float lo(f2 v) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-  (void)b;
-  return a;
-}
-__device__ __forceinline__ float hi(f2 v) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-  (void)a;
-  return b;
-}
+__device__ __forceinline__ float lo(f2 v) { return __uint_as_float((unsigned)(v & 0xffffffffull)); }
+__device__ __forceinline__ float hi(f2 v) { return __uint_as_float((unsigned)(v >> 32)); }
 __device__ __forceinline__ f2 sub2(f2 a, f2 b) {
   f2 r;
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -89,10 +80,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // Gaussian: d2 = dx*dx; d2 = fma(dy,dy,d2); d2 = fma(dz,dz,d2); t = 2^-d2
 // RQ:       w = fma(dx,dx,1); w = fma(dy,dy,w); w = fma(dz,dz,w); t = rcp(w*w)
 template <int KIND>
-__device__ __forceinline__ f2 term_pair(f2 ux, f2 uy, f2 uz, f2 vx, f2 vy, f2 vz) {
-  f2 dx = sub2(ux, vx);
-  f2 dy = sub2(uy, vy);
-  f2 dz = sub2(uz, vz);
+__device__ __forceinline__ f2 term_from_diffs(f2 dx, f2 dy, f2 dz) {
   if (KIND == kGaussian) {
     f2 s = mul2(dx, dx);
     s = fma2(dy, dy, s);
@@ -108,9 +96,22 @@ __device__ __forceinline__ f2 term_pair(f2 ux, f2 uy, f2 uz, f2 vx, f2 vy, f2 vz
   }
 }
 
+template <int KIND>
+__device__ __forceinline__ f2 term_pair(f2 ux, f2 uy, f2 uz, f2 vx, f2 vy, f2 vz) {
+  return term_from_diffs<KIND>(sub2(ux, vx), sub2(uy, vy), sub2(uz, vz));
+}
+
 // Sum over the M control points of one (query, support) pair, in the fixed order
 // (t0 + t2 + t4 + ...) + (t1 + t3 + ...): the canonical K_FK numerator shared by all kernels.
 __device__ __forceinline__ float pair_sum(f2 acc) { return lo(acc) + hi(acc); }
+
+// fp32 -> fp64 for x >= 0 on the integer (ALU) pipe: exact for normal x; x == 0 maps to
+// 2^-127 (< 6e-39, far below any tolerance). cvt.f64.f32 (F2F) would issue on the MUFU
+// pipe that bounds this kernel (measured: tools/precision_probe.cu), this does not.
+__device__ __forceinline__ double nonneg_f32_to_f64(float x) {
+  const uint32_t b = __float_as_uint(x);
+  return __hiloint2double((int)((b >> 3) + 0x38000000u), (int)(b << 29));
+}
 
 // ---------------------------------------------------------------------------------
 // mbarrier + TMA bulk copy (cp.async.bulk global -> shared), CTA scope

@@ -12,10 +12,11 @@
 //    f32x2 pairs; every support record is a warp-broadcast LDS.128 + LDS.64 shared
 //    by the QT queries. Per control-point pair: 3 FADD2 + FMUL2 + 2 FFMA2 +
 //    2 MUFU (ex2 or rcp) + FADD2 — MUFU-bound (one SFU op per term).
-//  * Accumulation: per support the M terms are summed in fp32 (fixed order), the
-//    alpha-weighted sum of 8 supports is an fp32 FFMA chain, folded into an fp64
-//    accumulator per query (DESIGN.md §5 error budget). 1/M is applied once at the
-//    end in fp64.
+//  * Accumulation: per support the M terms are summed in two fp32 lanes (even and odd
+//    control points, fixed order); both lane sums go to fp64 on the ALU pipe and are
+//    added to the query's fp64 score with alpha (stored as double) by DFMA — no fp32
+//    rounding above the 4-term lane sums (DESIGN.md §5 error budget). 1/M is applied
+//    once at the end in fp64.
 //  * Grid = query blocks x support splits, the split count chosen to fill 148 SMs in
 //    whole waves; splits > 1 write fp64 partials that a second kernel adds in a fixed
 //    order (deterministic).
@@ -24,9 +25,15 @@
 
 namespace fastron {
 
+#ifndef FASTRON_REORDER
+#define FASTRON_REORDER 1
+#endif
+#ifndef FASTRON_ACC_SPLIT
+#define FASTRON_ACC_SPLIT 1
+#endif
+
 constexpr int kNT = 128;     // threads per scoring CTA
 constexpr int kStages = 3;   // TMA ring depth
-constexpr int kGroup = 8;    // supports per fp32 partial before the fp64 fold
 
 __host__ __device__ constexpr int qt_for(int mp) { return mp <= 4 ? 8 : mp <= 8 ? 4 : mp <= 16 ? 2 : 1; }
 
@@ -58,7 +65,7 @@ __global__ void pack_kernel(const float4* __restrict__ spos, int64_t lds, const 
     reinterpret_cast<float4*>(rec + p * 8)[0] = make_float4(ax, bx, ay, by);
     reinterpret_cast<float4*>(rec + p * 8)[1] = make_float4(az, bz, 0.f, 0.f);
   }
-  T[(int64_t)kTileSupports * (MP / 2) * 8 + s] = (live && alpha) ? alpha[i] : 0.0f;
+  reinterpret_cast<double*>(T + tile_record_floats(MP))[s] = (live && alpha) ? (double)alpha[i] : 0.0;
 }
 
 cudaError_t launch_pack(const float4* spos, int64_t lds, const float* alpha, int64_t ns, int M, float scale,
@@ -235,33 +242,49 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
     const int st = it % kStages;
     mbar_wait(&bars[st], (uint32_t)((it / kStages) & 1));
     const float* T = stages + st * TF;
-    const float* alpha = T + kTileSupports * NP * 8;
-#pragma unroll 1
-    for (int g = 0; g < kTileSupports; g += kGroup) {
-      float part[QT];
-#pragma unroll
-      for (int j = 0; j < QT; ++j) part[j] = 0.0f;
+    const double* alpha = reinterpret_cast<const double*>(T + tile_record_floats(MP));
 #pragma unroll 2
-      for (int u = 0; u < kGroup; ++u) {
-        const float* rec = T + (g + u) * NP * 8;
-        f2 acc[QT];
+    for (int s = 0; s < kTileSupports; ++s) {
+      const float* rec = T + s * NP * 8;
+      f2 acc[QT];
 #pragma unroll
-        for (int p = 0; p < NP; ++p) {
-          const float4 xy = *reinterpret_cast<const float4*>(rec + p * 8);
-          const float2 zz = *reinterpret_cast<const float2*>(rec + p * 8 + 4);
-          const f2 vx = pk(xy.x, xy.y), vy = pk(xy.z, xy.w), vz = pk(zz.x, zz.y);
+      for (int p = 0; p < NP; ++p) {
+        const float4 xy = *reinterpret_cast<const float4*>(rec + p * 8);
+        const float2 zz = *reinterpret_cast<const float2*>(rec + p * 8 + 4);
+        const f2 vx = pk(xy.x, xy.y), vy = pk(xy.z, xy.w), vz = pk(zz.x, zz.y);
+#if FASTRON_REORDER
+        // coordinate-major order: consecutive instructions share the support operand,
+        // letting the operand-reuse cache absorb one register-bank read per FADD2
+        f2 dx[QT], dy[QT], dz[QT];
 #pragma unroll
-          for (int j = 0; j < QT; ++j) {
-            const f2 t = term_pair<KIND>(ux[j][p], uy[j][p], uz[j][p], vx, vy, vz);
-            acc[j] = p == 0 ? t : add2(acc[j], t);
-          }
+        for (int j = 0; j < QT; ++j) dx[j] = sub2(ux[j][p], vx);
+#pragma unroll
+        for (int j = 0; j < QT; ++j) dy[j] = sub2(uy[j][p], vy);
+#pragma unroll
+        for (int j = 0; j < QT; ++j) dz[j] = sub2(uz[j][p], vz);
+#pragma unroll
+        for (int j = 0; j < QT; ++j) {
+          const f2 t = term_from_diffs<KIND>(dx[j], dy[j], dz[j]);
+          acc[j] = p == 0 ? t : add2(acc[j], t);
         }
-        const float a = alpha[g + u];
+#else
 #pragma unroll
-        for (int j = 0; j < QT; ++j) part[j] = __fmaf_rn(a, pair_sum(acc[j]), part[j]);
+        for (int j = 0; j < QT; ++j) {
+          const f2 t = term_pair<KIND>(ux[j][p], uy[j][p], uz[j][p], vx, vy, vz);
+          acc[j] = p == 0 ? t : add2(acc[j], t);
+        }
+#endif
       }
+      const double a = alpha[s];
 #pragma unroll
-      for (int j = 0; j < QT; ++j) f[j] += (double)part[j];
+      for (int j = 0; j < QT; ++j) {
+#if FASTRON_ACC_SPLIT
+        f[j] = fma(a, nonneg_f32_to_f64(lo(acc[j])), f[j]);
+        f[j] = fma(a, nonneg_f32_to_f64(hi(acc[j])), f[j]);
+#else
+        f[j] = fma(a, nonneg_f32_to_f64(pair_sum(acc[j])), f[j]);
+#endif
+      }
     }
     __syncthreads();  // every thread is done with stage st
     if (tid == 0 && it + kStages < nt) {
