@@ -105,10 +105,8 @@ class ClockSampler:
 
 
 def _dist():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    from paper_1910_06451_b200 import dist as fd
+    return fd.world()
 
 
 def cpu_baseline(wl, target_s=12.0):
@@ -270,7 +268,8 @@ def run_ours(args):
     fb.load_library()
     wl = W.score_workload("headline", kind=args.kind)
     Q, S, M = len(wl.queries), len(wl.supports), wl.robot.n_cp
-    queries = wl.queries if rank == 0 else W.uniform_configs(np.random.default_rng(1000 + rank), Q, wl.robot.dof)
+    from paper_1910_06451_b200 import dist as fd
+    queries = fd.shard_queries(wl.queries, rank)  # weak scaling: every rank its own batch
     robot = fb.make_robot_struct(wl.robot)
     st = torch.cuda.current_stream()
 
@@ -316,12 +315,8 @@ def run_ours(args):
     ms_total = t0.elapsed_time(t1)
     fk_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
     sc_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
-    ms_step = ms_total / args.steps
-    if ws > 1:
-        t = torch.tensor([ms_step], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_step = float(t.item())
-    value = ws * Q / (ms_step * 1e-3)
+    ms_step = fd.max_over_ranks(ms_total / args.steps, device="cuda")
+    value = fd.aggregate_rate(Q, ws, ms_step)
     clocks = clk.summary()
 
     # ---- end to end through the public API with host buffers (pinned), rank-local ----
@@ -344,11 +339,7 @@ def run_ours(args):
         e2e_step()
     e1.record(st)
     e1.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / args.steps
-    if ws > 1:
-        t = torch.tensor([e2e_ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = fd.max_over_ranks(e0.elapsed_time(e1) / args.steps, device="cuda")
     assert np.array_equal(sh.numpy(), score.cpu().numpy()), "fastron_query disagrees with fk + score_packed"
 
     # ---- roofline of the dominant kernel (the score launch) ----
@@ -393,7 +384,7 @@ def run_ours(args):
                 "kernel_evals_per_s": value * S,
                 "roofline": roof,
                 "cpu_baseline": base,
-                "e2e": {"value": ws * Q / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": Q * wl.robot.dof * 4,
+                "e2e": {"value": fd.aggregate_rate(Q, ws, e2e_ms), "unit": UNIT, "h2d_bytes_per_step": Q * wl.robot.dof * 4,
                         "d2h_bytes_per_step": Q * 5, "ms_per_step": e2e_ms,
                         "api": "fastron_query with pinned host q/score/label"},
                 "gpu_launches": launches,

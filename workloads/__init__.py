@@ -8,7 +8,7 @@ geometry routine (capsule vs axis-aligned cube) that takes segment end points as
 product's FK in bench.py).
 
 Recipes follow BASELINE.json `configs` and the readings in DESIGN.md §3 (R4, R7, R12,
-R13, R14, R15). Every array is generated in float64 and rounded once to float32 (R15);
+R14, R15, R21). Every array is generated in float64 and rounded once to float32 (R15);
 the oracle promotes those exact float32 values back to float64.
 
 Seeds: cfg k uses numpy.random.default_rng(k); the headline uses 6. The 7-DOF arm
@@ -250,7 +250,7 @@ def train_workload(n: Optional[int] = None) -> TrainWorkload:
 
 
 def cfg5_gram_workload(n: Optional[int] = None):
-    """cfg5 Gram rebuild (R13): 6 cubes, 3 of them moved by 0.1 m in seeded random
+    """cfg5 Gram rebuild (R21): 6 cubes, 3 of them moved by 0.1 m in seeded random
     directions, then a fresh seeded set of 20,000 configurations whose M=16 Gram is
     rebuilt. Returns (robot, X, cubes_before, cubes_after)."""
     rng = np.random.default_rng(55)
