@@ -1,23 +1,37 @@
 // gram.cu — K3, the FK-kernel Gram matrix K_ij = K_FK(X_i, X_j) (
-// Algorithm 1 line "computeKernelMatrixColumn").
+// Algorithm 1's "computeKernelMatrixColumn").
 //
-// Upper-triangular 128x128 tiles, one CTA per tile (bi <= bj). The 128 column points
-// arrive as two packed support tiles by TMA bulk copy; each of the 256 threads holds
-// 2 row points in registers and evaluates 2 x 32 entries with the same term_pair()
-// as the scoring kernel, so K_ij is bit-identical to fastron_score with alpha = e_i
-// (the sum over m in the same order, then the exact 1/M for M a power of two).
-// The tile is staged in shared memory (row stride 129 floats: conflict-free
-// transposed reads) and written twice with coalesced stores: as (bi, bj) and, off the
-// diagonal, transposed as (bj, bi). K is therefore exactly symmetric and its diagonal
-// is exactly 1 (d^2 = 0 gives 2^0 = rcp(1) = 1).
+// Upper-triangular 128x128 tiles (bi <= bj), one CTA of 4 warps per tile:
+//  * COLUMN points live in registers: each lane holds CPL columns (4 at M <= 8, 2 at
+//    M <= 16) as pre-scaled f32x2 control-point pairs (the packed records of the
+//    scoring kernel); a warp covers 32*CPL columns;
+//  * the tile's 128 ROW points arrive as two packed support tiles by one TMA bulk copy;
+//    each warp walks a contiguous row range; a row record is a warp-broadcast
+//    LDS.128 + LDS.64 shared by the lane's CPL columns;
+//  * the (bi, bj) block is stored straight from registers: for a fixed row the 32 lanes
+//    write 32 consecutive floats (coalesced). The mirrored (bj, bi) block goes through a
+//    per-warp (32*CPL)x9 shared-memory transpose buffer, 8 rows at a time, and is written
+//    as one 32-byte segment (two float4) per column.
+// The same term_pair() and control-point summation order as fastron_score make K_ij
+// bit-identical to fastron_score(alpha = e_i) for M a power of two; K is exactly
+// symmetric (each unordered pair is computed once, or as the exact mirror image on
+// diagonal tiles), and K_ii = 1 exactly (d^2 = 0 gives 2^0 = rcp(1) = 1).
 #include "fastron_device.cuh"
 #include "internal.h"
 
 namespace fastron {
 
-constexpr int kGT = 256;   // threads per Gram CTA
-constexpr int kGB = 128;   // tile edge (2 support tiles)
-constexpr int kGS = kGB + 1;
+#ifndef FASTRON_GRAM_WARPS
+#define FASTRON_GRAM_WARPS 4
+#endif
+#ifndef FASTRON_GRAM_CPL8
+#define FASTRON_GRAM_CPL8 4
+#endif
+constexpr int kGT = 32 * FASTRON_GRAM_WARPS;  // threads per Gram CTA
+constexpr int kGW = kGT / 32;
+constexpr int kGB = 128;             // tile edge (2 support tiles)
+constexpr int kChunkRows = 8;        // rows per mirror-transpose chunk
+constexpr int kMS = kChunkRows + 1;  // padded stride of the transpose buffer
 
 __device__ __forceinline__ void tile_coords(int64_t t, int64_t nb, int64_t& bi, int64_t& bj) {
   // row-major enumeration of the upper triangle: row bi holds tiles bi..nb-1
@@ -30,44 +44,54 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t nb, int64_t& bi, 
   bj = r + (t - start(r));
 }
 
+__host__ __device__ constexpr int gram_cpl(int mp) {  // columns per lane
+  return mp <= 8 ? FASTRON_GRAM_CPL8 : mp <= 16 ? (FASTRON_GRAM_CPL8 < 2 ? FASTRON_GRAM_CPL8 : 2) : 1;
+}
+
 template <int MP, int KIND>
 __global__ void __launch_bounds__(kGT) gram_kernel(const float* __restrict__ packed, int64_t n, int M, int m_pow2,
                                                    float inv_m, float* __restrict__ K, int64_t ldk) {
   constexpr int NP = MP / 2;
+  constexpr int CPL = gram_cpl(MP);           // columns per lane
+  constexpr int WC = 32 * CPL;                // columns per warp
+  constexpr int G = kGB / WC;                 // column groups (warps sharing a row range)
+  constexpr int R = kGW / G;                  // row groups
+  constexpr int RW = kGB / R;                 // rows per warp (contiguous)
   constexpr int64_t TF = tile_floats(MP);
   constexpr uint32_t TB = (uint32_t)tile_bytes(MP);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
-  float* cols = reinterpret_cast<float*>(smem_raw + 128);      // 2 packed tiles
-  float* Ks = cols + 2 * TF;                                    // [128][129]
+  float* rows = reinterpret_cast<float*>(smem_raw + 128);  // 2 packed tiles
+  float* tbuf = rows + 2 * TF;                               // [kGW][WC][kMS]
 
   const int64_t nb = (n + kGB - 1) / kGB;
   int64_t bi, bj;
   tile_coords(blockIdx.x, nb, bi, bj);
   const int64_t i0 = bi * kGB, j0 = bj * kGB;
   const int64_t n_tiles = (n + kTileSupports - 1) / kTileSupports;
-  const int ct = (n_tiles - 2 * bj) >= 2 ? 2 : 1;  // column tiles present
+  const int rt = (n_tiles - 2 * bi) >= 2 ? 2 : 1;  // row tiles present
 
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cg = warp % G, rg = warp / G;
+  const int cbase = cg * WC;   // first column of this warp (tile-relative)
+  const int rbase = rg * RW;   // first row of this warp (tile-relative)
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_barrier_init();
   }
   __syncthreads();
   if (tid == 0) {
-    mbar_expect_tx(bar, TB * ct);
-    for (int c = 0; c < ct; ++c) tma_bulk_g2s(cols + c * TF, packed + (2 * bj + c) * TF, TB, bar);
+    mbar_expect_tx(bar, TB * rt);
+    for (int c = 0; c < rt; ++c) tma_bulk_g2s(rows + c * TF, packed + (2 * bi + c) * TF, TB, bar);
   }
 
-  // rows r and r + 64 of the row block, read from the same packed (scaled) records
-  const int r = tid & 63;
-  const int cg = tid >> 6;  // column group of 32
-  f2 ux[2][NP], uy[2][NP], uz[2][NP];
+  // the lane's CPL columns, read from the same packed (scaled) records
+  f2 ux[CPL][NP], uy[CPL][NP], uz[CPL][NP];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int64_t i = i0 + r + 64 * h;
-    const int64_t ii = i < n ? i : 0;
-    const float* rec = packed + (ii / kTileSupports) * TF + (ii % kTileSupports) * NP * 8;
+  for (int h = 0; h < CPL; ++h) {
+    const int64_t j = j0 + cbase + lane + 32 * h;
+    const int64_t jj = j < n ? j : 0;
+    const float* rec = packed + (jj / kTileSupports) * TF + (jj % kTileSupports) * NP * 8;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       const float4 xy = __ldg(reinterpret_cast<const float4*>(rec + p * 8));
@@ -79,57 +103,70 @@ __global__ void __launch_bounds__(kGT) gram_kernel(const float* __restrict__ pac
   }
   mbar_wait(bar, 0);
 
+  const bool mirror = bi != bj;
+  float* tb = tbuf + warp * (WC * kMS);
+  const int rows_here = (int)min((int64_t)kGB, n - i0);
+  for (int q0 = 0; q0 < RW; q0 += kChunkRows) {
+    if (rbase + q0 >= rows_here) break;  // warp-uniform
 #pragma unroll 2
-  for (int cc = 0; cc < 32; ++cc) {
-    const int c = cg * 32 + cc;
-    const float* rec = cols + (c / kTileSupports) * TF + (c % kTileSupports) * NP * 8;
-    f2 acc[2];
+    for (int qq = 0; qq < kChunkRows; ++qq) {
+      const int r = rbase + q0 + qq;
+      if (r >= rows_here) break;  // warp-uniform
+      const float* rec = rows + (r / kTileSupports) * TF + (r % kTileSupports) * NP * 8;
+      f2 acc[CPL];
 #pragma unroll
-    for (int p = 0; p < NP; ++p) {
-      const float4 xy = *reinterpret_cast<const float4*>(rec + p * 8);
-      const float2 zz = *reinterpret_cast<const float2*>(rec + p * 8 + 4);
-      const f2 vx = pk(xy.x, xy.y), vy = pk(xy.z, xy.w), vz = pk(zz.x, zz.y);
+      for (int p = 0; p < NP; ++p) {
+        const float4 xy = *reinterpret_cast<const float4*>(rec + p * 8);
+        const float2 zz = *reinterpret_cast<const float2*>(rec + p * 8 + 4);
+        const f2 vx = pk(xy.x, xy.y), vy = pk(xy.z, xy.w), vz = pk(zz.x, zz.y);
+        f2 dx[CPL], dy[CPL], dz[CPL];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const f2 t = term_pair<KIND>(ux[h][p], uy[h][p], uz[h][p], vx, vy, vz);
-        acc[h] = p == 0 ? t : add2(acc[h], t);
+        for (int h = 0; h < CPL; ++h) dx[h] = sub2(ux[h][p], vx);
+#pragma unroll
+        for (int h = 0; h < CPL; ++h) dy[h] = sub2(uy[h][p], vy);
+#pragma unroll
+        for (int h = 0; h < CPL; ++h) dz[h] = sub2(uz[h][p], vz);
+#pragma unroll
+        for (int h = 0; h < CPL; ++h) {
+          const f2 t = term_from_diffs<KIND>(dx[h], dy[h], dz[h]);
+          acc[h] = p == 0 ? t : add2(acc[h], t);
+        }
+      }
+      float* Krow = K + (i0 + r) * ldk + j0 + cbase;
+#pragma unroll
+      for (int h = 0; h < CPL; ++h) {
+        const float ks = pair_sum(acc[h]);
+        const float v = m_pow2 ? ks * inv_m : __fdiv_rn(ks, (float)M);
+        const int c = lane + 32 * h;
+        if (j0 + cbase + c < n) Krow[c] = v;  // direct block, coalesced across the warp
+        tb[c * kMS + qq] = v;                  // transposed copy for the mirror block
       }
     }
+    if (mirror) {
+      __syncwarp();
+      // mirror block: row j0 + cbase + c, columns i0 + rbase + q0 .. +7 (one 32-byte segment)
+      const int nrow = min(kChunkRows, rows_here - (rbase + q0));
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const float ks = pair_sum(acc[h]);
-      Ks[(r + 64 * h) * kGS + c] = m_pow2 ? ks * inv_m : __fdiv_rn(ks, (float)M);
-    }
-  }
-  __syncthreads();
-
-  // coalesced stores: tile (bi, bj) row by row, then its transpose as (bj, bi)
-  const int lane = tid & 31, warp = tid >> 5;
-  for (int rr = warp; rr < kGB; rr += kGT / 32) {
-    const int64_t i = i0 + rr;
-    if (i >= n) break;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int c = lane + 32 * q;
-      if (j0 + c < n) K[i * ldk + j0 + c] = Ks[rr * kGS + c];
-    }
-  }
-  if (bi != bj) {
-    for (int c = warp; c < kGB; c += kGT / 32) {
-      const int64_t j = j0 + c;
-      if (j >= n) break;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int rr = lane + 32 * q;
-        if (i0 + rr < n) K[j * ldk + i0 + rr] = Ks[rr * kGS + c];
+      for (int h = 0; h < CPL; ++h) {
+        const int c = lane + 32 * h;
+        if (j0 + cbase + c >= n) continue;
+        float* Kr = K + (j0 + cbase + c) * ldk + i0 + rbase + q0;
+        const float* src = tb + c * kMS;
+        if (nrow == kChunkRows && ((reinterpret_cast<uintptr_t>(Kr) & 15) == 0)) {
+          reinterpret_cast<float4*>(Kr)[0] = make_float4(src[0], src[1], src[2], src[3]);
+          reinterpret_cast<float4*>(Kr)[1] = make_float4(src[4], src[5], src[6], src[7]);
+        } else {
+          for (int qq = 0; qq < nrow; ++qq) Kr[qq] = src[qq];
+        }
       }
+      __syncwarp();
     }
   }
 }
 
 template <int MP, int KIND>
 static cudaError_t run_gram(const float* packed, int64_t n, int M, float* K, int64_t ldk, cudaStream_t st) {
-  const size_t smem = 128 + 2 * tile_bytes(MP) + (size_t)kGB * kGS * 4;
+  const size_t smem = 128 + 2 * tile_bytes(MP) + (size_t)kGW * 32 * gram_cpl(MP) * kMS * 4;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gram_kernel<MP, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

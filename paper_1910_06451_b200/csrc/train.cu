@@ -227,6 +227,16 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
   int64_t nnz = 0;
   for (int r = 0; r < C; ++r) nnz += *cluster.map_shared_rank(&s_cta_cnt[0], r);
 
+  // loop invariants: clamped K-row offsets of the slots and the label sign bit of each
+  // slot as an fp64 high-word mask (y_j fl(d K) is fl(d K) with its sign flipped)
+  int koff[EPT];
+  uint32_t sgn[EPT];
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    koff[k] = min(k * kTrainNT + tid, jlast);
+    sgn[k] = ((yneg >> k) & 1u) << 31;
+  }
+
   int64_t iters = 0, n_add = 0, n_remove = 0;
   int upd_i = -1;  // row of the pending rank-one update of F
   double upd_delta = 0.0;
@@ -240,7 +250,7 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
     if (have_upd) {
       const float* Krow = A.K + (int64_t)upd_i * A.ldk + lo;
 #pragma unroll
-      for (int k = 0; k < EPT; ++k) kr[k] = ld_evict_last(Krow + min(k * kTrainNT + tid, jlast), pol);
+      for (int k = 0; k < EPT; ++k) kr[k] = ld_evict_last(Krow + koff[k], pol);
     }
     double m0 = INFINITY, m1 = INFINITY;  // two interleaved chains (even / odd k)
     int k0 = -1, k1 = -1;
@@ -248,7 +258,8 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
     for (int k = 0; k < EPT; ++k) {
       if (have_upd) {
         const double p = __dmul_rn(upd_delta, (double)kr[k]);
-        G[k] = ((yneg >> k) & 1u) ? __dsub_rn(G[k], p) : __dadd_rn(G[k], p);  // Eq. 8, signed
+        const double sp = __hiloint2double(__double2hiint(p) ^ (int)sgn[k], __double2loint(p));  // y_j p
+        G[k] = __dadd_rn(G[k], sp);  // Eq. 8, signed
       }
       if (k & 1) {
         if (G[k] < m1) { m1 = G[k]; k1 = k; }

@@ -4,7 +4,8 @@ import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_1910_06451_b200 as fb, workloads as W
-tw = W.train_workload()
+N = int(os.environ.get("TRAIN_N", "5000"))
+tw = W.train_workload(N)
 pos = fb.fastron_fk(tw.robot, torch.from_numpy(tw.X).cuda())
 P = np.transpose(pos.cpu().numpy()[:, :, :3], (1, 0, 2)).astype(np.float64)
 y = torch.from_numpy(W.capsule_aabb_labels(W.chain_points(P), tw.cubes, tw.radius)).cuda()
