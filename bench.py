@@ -234,6 +234,36 @@ def _time_rows(fb, torch, kind):
     res = fb.train_result(out["result"])
     rows["cfg3_train"] = {"ms": ms, **res, "us_per_iteration": ms * 1e3 / max(res["iterations"], 1),
                           "positive_fraction": float((y > 0).float().mean().item())}
+    # cfg5: M = 16 scoring (1M of the 10M queries x 20k supports) and the 20k x 20k Gram rebuild (R21)
+    wl = W.score_workload("cfg5", n_queries=1_000_000)
+    spos = fb.fastron_fk(wl.robot, torch.from_numpy(wl.supports).cuda())
+    model = fb.fastron_model_pack(spos, torch.from_numpy(wl.alpha).cuda(), kind, wl.gamma)
+    q = torch.from_numpy(wl.queries).cuda()
+    qpos = torch.empty((16, len(wl.queries), 4), device="cuda")
+    sc = torch.empty(len(wl.queries), device="cuda")
+    lb = torch.empty(len(wl.queries), dtype=torch.int8, device="cuda")
+
+    def step5():
+        fb.fastron_fk(wl.robot, q, pos=qpos)
+        fb.fastron_score_packed(qpos, model, sc, lb)
+
+    ms = timed(step5, 3)
+    terms = len(wl.queries) * len(wl.supports) * 16
+    rows["cfg5_score_1M"] = {"ms": ms, "checks_per_s": len(wl.queries) / ms * 1e3,
+                             "kernel_evals_per_s": len(wl.queries) * len(wl.supports) / ms * 1e3,
+                             "mufu_frac": terms / (ms * 1e-3) / (148 * 16 * 1.965e9)}
+    del qpos, q, sc, lb
+    robot5, X5, _, _ = W.cfg5_gram_workload()
+    pos5 = fb.fastron_fk(robot5, torch.from_numpy(X5).cuda())
+    n5 = len(X5)
+    K5 = torch.empty((n5, n5), device="cuda")
+    gws5 = torch.empty(fb.load_library().fastron_gram_workspace_bytes(n5, 16), dtype=torch.uint8, device="cuda")
+    ms = timed(lambda: fb.fastron_gram(pos5, kind, 5.0, K=K5, workspace=gws5), 3)
+    nb = (n5 + 127) // 128
+    rows["cfg5_gram"] = {"ms": ms, "n": n5, "mufu_frac": nb * (nb + 1) // 2 * 128 * 128 * 16 / (ms * 1e-3) / (148 * 16 * 1.965e9),
+                         "write_GBps": n5 * n5 * 4 / ms * 1e-6}
+    del K5
+    torch.cuda.empty_cache()
     # cfg4: 10k edges x 64 points, 3k supports, early exit
     ew = W.edge_workload()
     spos = fb.fastron_fk(ew.robot, torch.from_numpy(ew.supports).cuda())
