@@ -106,12 +106,13 @@ __global__ void __launch_bounds__(kGT) gram_kernel(const float* __restrict__ pac
   const bool mirror = bi != bj;
   float* tb = tbuf + warp * (WC * kMS);
   const int rows_here = (int)min((int64_t)kGB, n - i0);
-  for (int q0 = 0; q0 < RW; q0 += kChunkRows) {
-    if (rbase + q0 >= rows_here) break;  // warp-uniform
+  // fixed trip counts (no early exits) so loads of the next row overlap this row's math;
+  // rows past the matrix edge are computed on stale shared memory but never stored
+  const int q_end = min(RW, ((rows_here - rbase + kChunkRows - 1) / kChunkRows) * kChunkRows);
+  for (int q0 = 0; q0 < q_end; q0 += kChunkRows) {
 #pragma unroll 2
     for (int qq = 0; qq < kChunkRows; ++qq) {
       const int r = rbase + q0 + qq;
-      if (r >= rows_here) break;  // warp-uniform
       const float* rec = rows + (r / kTileSupports) * TF + (r % kTileSupports) * NP * 8;
       f2 acc[CPL];
 #pragma unroll
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(kGT) gram_kernel(const float* __restrict__ pac
         const float ks = pair_sum(acc[h]);
         const float v = m_pow2 ? ks * inv_m : __fdiv_rn(ks, (float)M);
         const int c = lane + 32 * h;
-        if (j0 + cbase + c < n) Krow[c] = v;  // direct block, coalesced across the warp
+        if (r < rows_here && j0 + cbase + c < n) Krow[c] = v;  // direct block, coalesced across the warp
         tb[c * kMS + qq] = v;                  // transposed copy for the mirror block
       }
     }

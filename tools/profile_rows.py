@@ -26,6 +26,11 @@ for rep in range(2):
         sp = fb.fastron_fk(wl.robot, torch.from_numpy(wl.supports).cuda())
         qp = fb.fastron_fk(wl.robot, torch.from_numpy(wl.queries).cuda())
         fb.fastron_score(qp, sp, torch.from_numpy(wl.alpha).cuda(), 0, wl.gamma)
+if "gram5" in which:
+    robot5, X5, _, _ = W.cfg5_gram_workload(8192)
+    pos5 = fb.fastron_fk(robot5, torch.from_numpy(X5).cuda())
+    for rep in range(2):
+        fb.fastron_gram(pos5, 0, 5.0)
 torch.cuda.synchronize()
 if "train" in which:
     print(fb.train_result(out["result"]))
