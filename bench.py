@@ -264,6 +264,29 @@ def _time_rows(fb, torch, kind):
                          "write_GBps": n5 * n5 * 4 / ms * 1e-6}
     del K5
     torch.cuda.empty_cache()
+    # Table I context: Fastron FK (|S| = 303, M = 8) vs the joint-space "Fastron RBF" kernel
+    # (|S| = 2369), the paper's mean support-set sizes, 1M queries each
+    hw = W.score_workload("headline", n_queries=1_000_000)
+    qd = torch.from_numpy(hw.queries).cuda()
+    res_t1 = {}
+    for name, ns in (("fk", 303), ("rbf_joint", 2369)):
+        sup = torch.from_numpy(hw.supports[:ns]).cuda()
+        al = torch.from_numpy(hw.alpha[:ns]).cuda()
+        if name == "fk":
+            sp = fb.fastron_fk(hw.robot, sup)
+            mdl = fb.fastron_model_pack(sp, al, kind, hw.gamma)
+            qp = torch.empty((8, len(hw.queries), 4), device="cuda")
+            fn = lambda: (fb.fastron_fk(hw.robot, qd, pos=qp), fb.fastron_score_packed(qp, mdl))
+        else:
+            wsj = torch.empty(fb.load_library().fastron_score_joint_workspace_bytes(len(hw.queries), ns, 7),
+                              dtype=torch.uint8, device="cuda")
+            fn = lambda: fb.fastron_score_joint(qd, sup, al, kind, 0.5, workspace=wsj)
+        ms = timed(fn, 5)
+        res_t1[name] = {"n_supports": ns, "ms": ms, "checks_per_s": len(hw.queries) / ms * 1e3,
+                        "us_per_check_batched": ms * 1e3 / len(hw.queries)}
+    res_t1["fk_speedup_vs_rbf"] = res_t1["rbf_joint"]["ms"] / res_t1["fk"]["ms"]
+    res_t1["paper_query_us"] = {"fk": 2.5, "rbf": 4.6, "note": "PAPER.md:290-291, single queries, unstated CPU"}
+    rows["table1_query_sizes"] = res_t1
     # cfg4: 10k edges x 64 points, 3k supports, early exit
     ew = W.edge_workload()
     spos = fb.fastron_fk(ew.robot, torch.from_numpy(ew.supports).cuda())

@@ -193,6 +193,24 @@ fastron_status fastron_edge_check(const fastron_robot* robot, const float* qa, c
                                   void* workspace, size_t workspace_bytes, void* stream);
 
 /*
+ * fastron_score_joint / fastron_gram_joint — the joint-space RBF kernel of the paper's
+ * "Fastron RBF" baseline (Eq. 3, Table I): K(x, x') is ONE RBF term
+ * of the joint-vector distance ||x - x'||^2 (no forward kinematics, no mean), with the
+ * term of k.kind. Inputs are configurations, not positions.
+ *   q: device float [nq][ldq], s: device float [ns][lds], x: device float [n][ldx];
+ *   dof in [1, 16] (ldq, lds, ldx >= dof). alpha, score, label, K: as fastron_score /
+ *   fastron_gram. workspace: >= the matching *_workspace_bytes (256-byte aligned).
+ * fastron_train accepts the resulting K unchanged (the Alg. 1 update is kernel-agnostic).
+ */
+size_t fastron_score_joint_workspace_bytes(int64_t nq, int64_t ns, int32_t dof);
+fastron_status fastron_score_joint(const float* q, int64_t nq, int64_t ldq, const float* s, const float* alpha,
+                                   int64_t ns, int64_t lds, int32_t dof, fastron_kernel k, float* score,
+                                   int8_t* label, void* workspace, size_t workspace_bytes, void* stream);
+size_t fastron_gram_joint_workspace_bytes(int64_t n, int32_t dof);
+fastron_status fastron_gram_joint(const float* x, int64_t n, int64_t ldx, int32_t dof, fastron_kernel k, float* K,
+                                  int64_t ldk, void* workspace, size_t workspace_bytes, void* stream);
+
+/*
  * fastron_query — the configuration-level proxy collision check, fastron_fk followed
  * by fastron_score on the same stream ("query").
  *   q: float [nq][ldq], HOST (pageable or pinned) or DEVICE. score (nullable) and

@@ -63,6 +63,13 @@ def lib():
         L.oracle_edge.argtypes = [ctypes.c_int, dp, dp, ctypes.c_int, ip, dp, fp, fp, i64, ctypes.c_int,
                                   ctypes.c_int, ctypes.c_double, dp, dp, i64, u8, dp, dp]
         L.oracle_edge.restype = None
+        L.oracle_joint_kernel.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_int, fp, fp]
+        L.oracle_joint_kernel.restype = ctypes.c_double
+        L.oracle_score_joint.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_int, fp, i64, i64, fp, i64, i64, dp, dp,
+                                         i8]
+        L.oracle_score_joint.restype = None
+        L.oracle_gram_joint.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_int, fp, i64, i64, dp]
+        L.oracle_gram_joint.restype = None
         L.oracle_num_threads.argtypes = []
         L.oracle_num_threads.restype = ctypes.c_int
         _lib = L
@@ -194,3 +201,32 @@ def edge(robot, qa, qb, n_interp, kind, gamma, spos, alpha, with_all=False):
                       E, int(n_interp), int(kind), float(gamma), _p(spos, ctypes.c_double), _p(alpha, ctypes.c_double),
                       spos.shape[0], _p(hit, ctypes.c_uint8), _p(fmax, ctypes.c_double), _p(fall, ctypes.c_double))
     return hit, fmax, fall
+
+
+def joint_kernel(kind, gamma, x, xp) -> float:
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+    xp = np.ascontiguousarray(np.asarray(xp, dtype=np.float32))
+    return float(lib().oracle_joint_kernel(int(kind), float(gamma), x.shape[0], _p(x, ctypes.c_float),
+                                           _p(xp, ctypes.c_float)))
+
+
+def score_joint(kind, gamma, q, s, alpha):
+    """Joint-space RBF ("Fastron RBF") scores of fp32 configurations q (nq, D) vs supports s (ns, D)."""
+    q = np.ascontiguousarray(np.asarray(q, dtype=np.float32))
+    s = np.ascontiguousarray(np.asarray(s, dtype=np.float32))
+    alpha = np.ascontiguousarray(np.asarray(alpha, dtype=np.float32).astype(np.float64))
+    nq, D = q.shape
+    ns = s.shape[0]
+    f = np.zeros(nq)
+    lab = np.zeros(nq, dtype=np.int8)
+    lib().oracle_score_joint(int(kind), float(gamma), D, _p(q, ctypes.c_float), nq, D, _p(s, ctypes.c_float), ns, D,
+                             _p(alpha, ctypes.c_double), _p(f, ctypes.c_double), _p(lab, ctypes.c_int8))
+    return f, lab
+
+
+def gram_joint(kind, gamma, x) -> np.ndarray:
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+    n, D = x.shape
+    K = np.zeros((n, n))
+    lib().oracle_gram_joint(int(kind), float(gamma), D, _p(x, ctypes.c_float), n, D, _p(K, ctypes.c_double))
+    return K

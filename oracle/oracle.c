@@ -25,6 +25,7 @@
  *   oracle_train         — hand-derived 2-point traces (tests/golden/), Claim 2
  *                          loss decrease, sign constraint, F = K alpha audit
  *   oracle_edge          — a=b and endpoint cases; OR of per-point scores
+ *   oracle_*_joint       — RQ worked values on 7-D vectors; Fig. 2 equality; PD Gram
  * No function here is "parity unpinned".
  *
  * Build (also done by __graft_entry__.build()):
@@ -182,6 +183,35 @@ void oracle_gram(int kind, double gamma, int n_cp, const double* pos, int64_t n,
   for (int64_t i = 0; i < n; ++i)
     for (int64_t j = 0; j < n; ++j)
       K[i * n + j] = oracle_kernel_value(kind, gamma, n_cp, pos + i * n_cp * 3, pos + j * n_cp * 3);
+}
+
+/* Joint-space RBF kernel of the "Fastron RBF" baseline (Table I):
+ * K(x, x') = term(||x - x'||^2) on the raw D-dimensional joint vectors (fp32 inputs). */
+double oracle_joint_kernel(int kind, double gamma, int dof, const float* x, const float* xp) {
+  double d2 = 0.0;
+  for (int i = 0; i < dof; ++i) {
+    double d = (double)x[i] - (double)xp[i];
+    d2 += d * d;
+  }
+  return oracle_rbf_term(kind, gamma, d2);
+}
+
+/* f(x) = sum_i K(S_i, x) alpha_i with the joint-space kernel. */
+void oracle_score_joint(int kind, double gamma, int dof, const float* q, int64_t nq, int64_t ldq, const float* s,
+                        int64_t ns, int64_t lds, const double* alpha, double* f, int8_t* label) {
+#pragma omp parallel for schedule(static)
+  for (int64_t j = 0; j < nq; ++j) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < ns; ++i) acc += oracle_joint_kernel(kind, gamma, dof, s + i * lds, q + j * ldq) * alpha[i];
+    f[j] = acc;
+    if (label) label[j] = acc > 0.0 ? 1 : -1;
+  }
+}
+
+void oracle_gram_joint(int kind, double gamma, int dof, const float* x, int64_t n, int64_t ldx, double* K) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) K[i * n + j] = oracle_joint_kernel(kind, gamma, dof, x + i * ldx, x + j * ldx);
 }
 
 /* ------------------------------------------------------------------------ */

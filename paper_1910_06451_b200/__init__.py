@@ -29,7 +29,8 @@ EXPORTED = [
     "fastron_train_max_n", "fastron_train", "fastron_edge_workspace_bytes", "fastron_edge_check",
     "fastron_query_workspace_bytes", "fastron_query", "fastron_last_error", "fastron_version",
     "fastron_launch_count", "fastron_model_bytes", "fastron_model_pack", "fastron_score_packed_workspace_bytes",
-    "fastron_score_packed",
+    "fastron_score_packed", "fastron_score_joint_workspace_bytes", "fastron_score_joint",
+    "fastron_gram_joint_workspace_bytes", "fastron_gram_joint",
 ]
 
 
@@ -84,6 +85,12 @@ def load_library(path: str = LIB_PATH):
     L.fastron_score_packed_workspace_bytes.argtypes = [i64, i64, i32]
     L.fastron_score_packed_workspace_bytes.restype = sz
     L.fastron_score_packed.argtypes = [vp, i64, i64, vp, i64, i32, fastron_kernel, vp, vp, vp, sz, vp]
+    L.fastron_score_joint_workspace_bytes.argtypes = [i64, i64, i32]
+    L.fastron_score_joint_workspace_bytes.restype = sz
+    L.fastron_score_joint.argtypes = [vp, i64, i64, vp, vp, i64, i64, i32, fastron_kernel, vp, vp, vp, sz, vp]
+    L.fastron_gram_joint_workspace_bytes.argtypes = [i64, i32]
+    L.fastron_gram_joint_workspace_bytes.restype = sz
+    L.fastron_gram_joint.argtypes = [vp, i64, i64, i32, fastron_kernel, vp, i64, vp, sz, vp]
     L.fastron_gram_workspace_bytes.argtypes = [i64, i32]
     L.fastron_gram_workspace_bytes.restype = sz
     L.fastron_gram.argtypes = [vp, i64, i64, i32, fastron_kernel, vp, i64, vp, sz, vp]
@@ -97,7 +104,7 @@ def load_library(path: str = LIB_PATH):
     L.fastron_query_workspace_bytes.restype = sz
     L.fastron_query.argtypes = [rp, vp, i64, i64, vp, vp, i64, i64, fastron_kernel, vp, vp, vp, sz, vp]
     for f in ("fastron_fk", "fastron_score", "fastron_gram", "fastron_train", "fastron_edge_check", "fastron_query",
-              "fastron_model_pack", "fastron_score_packed"):
+              "fastron_model_pack", "fastron_score_packed", "fastron_score_joint", "fastron_gram_joint"):
         getattr(L, f).restype = st
     L.fastron_last_error.argtypes = []
     L.fastron_last_error.restype = ctypes.c_char_p
@@ -253,6 +260,42 @@ def fastron_gram(pos, kind: int, gamma: float, K=None, workspace=None, stream=No
         workspace = _workspace(need, pos.device)
     _check(L.fastron_gram(_ptr(pos), n, pos.stride(0) // 4, M, _kernel(kind, gamma), _ptr(K), K.stride(0),
                           _ptr(workspace), workspace.numel(), _stream(stream)))
+    return K
+
+
+def fastron_score_joint(q, s, alpha, kind: int, gamma: float, score=None, label=None, workspace=None, stream=None):
+    """Joint-space RBF ("Fastron RBF" baseline): q (nq, >=D), s (ns, >=D) configurations."""
+    import torch
+    L = load_library()
+    _require_cuda(q, s, alpha)
+    nq, ns = q.shape[0], s.shape[0]
+    dof = q.shape[1]
+    if score is None:
+        score = torch.empty(nq, dtype=torch.float32, device=q.device)
+    if label is None:
+        label = torch.empty(nq, dtype=torch.int8, device=q.device)
+    need = L.fastron_score_joint_workspace_bytes(nq, ns, dof)
+    if workspace is None or workspace.numel() < need:
+        workspace = _workspace(need, q.device)
+    _check(L.fastron_score_joint(_ptr(q), nq, q.stride(0), _ptr(s) if ns else None, _ptr(alpha) if ns else None, ns,
+                                 s.stride(0) if ns else dof, dof, _kernel(kind, gamma), _ptr(score), _ptr(label),
+                                 _ptr(workspace), workspace.numel(), _stream(stream)))
+    return score, label
+
+
+def fastron_gram_joint(x, kind: int, gamma: float, K=None, workspace=None, stream=None):
+    """Joint-space RBF Gram of configurations x (n, D)."""
+    import torch
+    L = load_library()
+    _require_cuda(x, K)
+    n, dof = x.shape[0], x.shape[1]
+    if K is None:
+        K = torch.empty((n, n), dtype=torch.float32, device=x.device)
+    need = L.fastron_gram_joint_workspace_bytes(n, dof)
+    if workspace is None or workspace.numel() < need:
+        workspace = _workspace(need, x.device)
+    _check(L.fastron_gram_joint(_ptr(x), n, x.stride(0), dof, _kernel(kind, gamma), _ptr(K), K.stride(0),
+                                _ptr(workspace), workspace.numel(), _stream(stream)))
     return K
 
 

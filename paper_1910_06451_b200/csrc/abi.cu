@@ -376,6 +376,77 @@ fastron_status fastron_edge_check(const fastron_robot* robot, const float* qa, c
   return FASTRON_OK;
 }
 
+size_t fastron_score_joint_workspace_bytes(int64_t nq, int64_t ns, int32_t dof) {
+  if (nq < 0 || ns < 0 || dof < 1 || dof > FASTRON_MAX_DOF) return 0;
+  const int Mj = joint_points(dof);
+  return align_up((size_t)(nq + ns) * Mj * 16) + align_up(packed_bytes(ns, Mj)) +
+         align_up(score_partial_bytes(nq, ns, Mj));
+}
+
+fastron_status fastron_score_joint(const float* q, int64_t nq, int64_t ldq, const float* sx, const float* alpha,
+                                   int64_t ns, int64_t lds, int32_t dof, fastron_kernel k, float* score,
+                                   int8_t* label, void* workspace, size_t workspace_bytes, void* stream) {
+  fastron_status s = check_kernel(k);
+  if (s != FASTRON_OK) return s;
+  FASTRON_REQUIRE(nq >= 0 && ns >= 0, "nq and ns must be >= 0");
+  FASTRON_REQUIRE(dof >= 1 && dof <= FASTRON_MAX_DOF, "dof must be in [1,16], got %d", dof);
+  if (nq == 0) return FASTRON_OK;
+  FASTRON_REQUIRE(q != nullptr && ldq >= dof, "q must be non-NULL with ldq >= dof");
+  FASTRON_REQUIRE(score || label, "score and label are both NULL");
+  if (ns > 0) FASTRON_REQUIRE(sx && alpha && lds >= dof, "s and alpha must be non-NULL with lds >= dof when ns > 0");
+  const size_t need = fastron_score_joint_workspace_bytes(nq, ns, dof);
+  if (workspace_bytes < need || !workspace)
+    return fail(FASTRON_ERR_WORKSPACE, "fastron_score_joint needs %zu workspace bytes, got %zu", need, workspace_bytes);
+  FASTRON_REQUIRE(((uintptr_t)workspace & 255) == 0, "workspace must be 256-byte aligned");
+  const int Mj = joint_points(dof);
+  char* ws = static_cast<char*>(workspace);
+  float4* qpts = reinterpret_cast<float4*>(ws);
+  float4* spts = qpts + (size_t)nq * Mj;
+  ws += align_up((size_t)(nq + ns) * Mj * 16);
+  float* packed = reinterpret_cast<float*>(ws);
+  ws += align_up(packed_bytes(ns, Mj));
+  double* partial = reinterpret_cast<double*>(ws);
+  cudaStream_t st = S(stream);
+  const float c = kernel_scale(k);
+  cudaError_t e = launch_joint_points(q, nq, ldq, dof, qpts, st);
+  if (e == cudaSuccess) e = launch_joint_points(sx, ns, lds, dof, spts, st);
+  if (e == cudaSuccess) e = launch_pack(spts, ns, alpha, ns, Mj, c, packed, st, true);
+  if (e == cudaSuccess) e = launch_score_joint(qpts, nq, packed, ns, dof, k.kind, c, score, label, partial, st);
+  return cuda_status(e, "fastron_score_joint");
+}
+
+size_t fastron_gram_joint_workspace_bytes(int64_t n, int32_t dof) {
+  if (n < 0 || dof < 1 || dof > FASTRON_MAX_DOF) return 0;
+  const int Mj = joint_points(dof);
+  const int64_t tiles = n_support_tiles(n);
+  return align_up((size_t)n * Mj * 16) + align_up(packed_bytes((tiles + 1) / 2 * 2 * kTileSupports, Mj));
+}
+
+fastron_status fastron_gram_joint(const float* x, int64_t n, int64_t ldx, int32_t dof, fastron_kernel k, float* K,
+                                  int64_t ldk, void* workspace, size_t workspace_bytes, void* stream) {
+  fastron_status s = check_kernel(k);
+  if (s != FASTRON_OK) return s;
+  FASTRON_REQUIRE(n >= 0, "n must be >= 0");
+  FASTRON_REQUIRE(dof >= 1 && dof <= FASTRON_MAX_DOF, "dof must be in [1,16], got %d", dof);
+  if (n == 0) return FASTRON_OK;
+  FASTRON_REQUIRE(x && K, "x and K must be non-NULL");
+  FASTRON_REQUIRE(ldx >= dof && ldk >= n, "ldx must be >= dof and ldk >= n");
+  const size_t need = fastron_gram_joint_workspace_bytes(n, dof);
+  if (workspace_bytes < need || !workspace)
+    return fail(FASTRON_ERR_WORKSPACE, "fastron_gram_joint needs %zu workspace bytes, got %zu", need, workspace_bytes);
+  FASTRON_REQUIRE(((uintptr_t)workspace & 255) == 0, "workspace must be 256-byte aligned");
+  const int Mj = joint_points(dof);
+  char* ws = static_cast<char*>(workspace);
+  float4* pts = reinterpret_cast<float4*>(ws);
+  float* packed = reinterpret_cast<float*>(ws + align_up((size_t)n * Mj * 16));
+  cudaStream_t st = S(stream);
+  const float c = kernel_scale(k);
+  cudaError_t e = launch_joint_points(x, n, ldx, dof, pts, st);
+  if (e == cudaSuccess) e = launch_pack(pts, n, nullptr, n, Mj, c, packed, st, true);
+  if (e == cudaSuccess) e = launch_gram_joint(packed, n, dof, k.kind, K, ldk, st);
+  return cuda_status(e, "fastron_gram_joint");
+}
+
 size_t fastron_query_workspace_bytes(int64_t nq, int64_t ns, int32_t n_cp, int32_t dof) {
   if (nq < 0 || ns < 0 || n_cp < 1 || n_cp > FASTRON_MAX_CP || dof < 1 || dof > FASTRON_MAX_DOF) return 0;
   const int64_t chunk = nq < kQueryChunk ? nq : kQueryChunk;

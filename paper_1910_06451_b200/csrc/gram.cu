@@ -12,6 +12,8 @@
 //    write 32 consecutive floats (coalesced). The mirrored (bj, bi) block goes through a
 //    per-warp (32*CPL)x9 shared-memory transpose buffer, 8 rows at a time, and is written
 //    as one 32-byte segment (two float4) per column.
+// JOINT = true builds the joint-space RBF Gram of the "Fastron RBF" baseline (PAPER.md:37,
+// :114-117) from zero-padded pseudo points: one RBF term of the whole squared distance.
 // The same term_pair() and control-point summation order as fastron_score make K_ij
 // bit-identical to fastron_score(alpha = e_i) for M a power of two; K is exactly
 // symmetric (each unordered pair is computed once, or as the exact mirror image on
@@ -48,7 +50,7 @@ __host__ __device__ constexpr int gram_cpl(int mp) {  // columns per lane
   return mp <= 8 ? FASTRON_GRAM_CPL8 : mp <= 16 ? (FASTRON_GRAM_CPL8 < 2 ? FASTRON_GRAM_CPL8 : 2) : 1;
 }
 
-template <int MP, int KIND>
+template <int MP, int KIND, bool JOINT>
 __global__ void __launch_bounds__(kGT) gram_kernel(const float* __restrict__ packed, int64_t n, int M, int m_pow2,
                                                    float inv_m, float* __restrict__ K, int64_t ldk) {
   constexpr int NP = MP / 2;
@@ -129,15 +131,32 @@ __global__ void __launch_bounds__(kGT) gram_kernel(const float* __restrict__ pac
         for (int h = 0; h < CPL; ++h) dz[h] = sub2(uz[h][p], vz);
 #pragma unroll
         for (int h = 0; h < CPL; ++h) {
-          const f2 t = term_from_diffs<KIND>(dx[h], dy[h], dz[h]);
-          acc[h] = p == 0 ? t : add2(acc[h], t);
+          if (JOINT) {  // squared joint-space distance, summed over all pseudo points
+            acc[h] = p == 0 ? mul2(dx[h], dx[h]) : fma2(dx[h], dx[h], acc[h]);
+            acc[h] = fma2(dy[h], dy[h], acc[h]);
+            acc[h] = fma2(dz[h], dz[h], acc[h]);
+          } else {
+            const f2 t = term_from_diffs<KIND>(dx[h], dy[h], dz[h]);
+            acc[h] = p == 0 ? t : add2(acc[h], t);
+          }
         }
       }
       float* Krow = K + (i0 + r) * ldk + j0 + cbase;
 #pragma unroll
       for (int h = 0; h < CPL; ++h) {
-        const float ks = pair_sum(acc[h]);
-        const float v = m_pow2 ? ks * inv_m : __fdiv_rn(ks, (float)M);
+        float v;
+        if (JOINT) {
+          const float d2 = pair_sum(acc[h]);
+          if (KIND == kGaussian) {
+            v = ex2_neg(d2);
+          } else {
+            const float w = 1.0f + d2;
+            v = rcp_approx(w * w);
+          }
+        } else {
+          const float ks = pair_sum(acc[h]);
+          v = m_pow2 ? ks * inv_m : __fdiv_rn(ks, (float)M);
+        }
         const int c = lane + 32 * h;
         if (r < rows_here && j0 + cbase + c < n) Krow[c] = v;  // direct block, coalesced across the warp
         tb[c * kMS + qq] = v;                  // transposed copy for the mirror block
@@ -165,21 +184,39 @@ __global__ void __launch_bounds__(kGT) gram_kernel(const float* __restrict__ pac
   }
 }
 
-template <int MP, int KIND>
+template <int MP, int KIND, bool JOINT = false>
 static cudaError_t run_gram(const float* packed, int64_t n, int M, float* K, int64_t ldk, cudaStream_t st) {
   const size_t smem = 128 + 2 * tile_bytes(MP) + (size_t)kGW * 32 * gram_cpl(MP) * kMS * 4;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gram_kernel<MP, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(gram_kernel<MP, KIND, JOINT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   const int64_t nb = (n + kGB - 1) / kGB;
   const int64_t tiles = nb * (nb + 1) / 2;
   if (tiles > 0x7fffffff) return cudaErrorInvalidValue;
   const int m_pow2 = (M & (M - 1)) == 0;
-  gram_kernel<MP, KIND><<<(unsigned)tiles, kGT, smem, st>>>(packed, n, M, m_pow2, 1.0f / (float)M, K, ldk);
+  gram_kernel<MP, KIND, JOINT><<<(unsigned)tiles, kGT, smem, st>>>(packed, n, M, m_pow2, 1.0f / (float)M, K, ldk);
   g_launches.fetch_add(1);
   return cudaGetLastError();
+}
+
+cudaError_t launch_gram_joint(const float* packed, int64_t n, int D, int kind, float* K, int64_t ldk, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int Mj = joint_points(D);
+  switch (padded_m(Mj)) {
+    case 2:
+      return kind == kGaussian ? run_gram<2, kGaussian, true>(packed, n, Mj, K, ldk, st)
+                               : run_gram<2, kRQ, true>(packed, n, Mj, K, ldk, st);
+    case 4:
+      return kind == kGaussian ? run_gram<4, kGaussian, true>(packed, n, Mj, K, ldk, st)
+                               : run_gram<4, kRQ, true>(packed, n, Mj, K, ldk, st);
+    case 6:
+      return kind == kGaussian ? run_gram<6, kGaussian, true>(packed, n, Mj, K, ldk, st)
+                               : run_gram<6, kRQ, true>(packed, n, Mj, K, ldk, st);
+    default:
+      return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_gram(const float* packed, int64_t n, int M, int kind, float* K, int64_t ldk, cudaStream_t st) {

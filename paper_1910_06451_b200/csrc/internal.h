@@ -28,7 +28,7 @@ int padded_m(int M);
 int64_t n_support_tiles(int64_t ns);
 size_t packed_bytes(int64_t ns, int M);
 cudaError_t launch_pack(const float4* spos, int64_t lds, const float* alpha, int64_t ns, int M, float scale,
-                        float* packed, cudaStream_t st);
+                        float* packed, cudaStream_t st, bool joint = false);
 
 // K2: scoring. Plan = grid decomposition (query blocks x support splits).
 struct ScorePlan {
@@ -62,6 +62,13 @@ struct EdgeRound {
 };
 cudaError_t launch_edge_round(const FkParams& P, const EdgeRound& R, const float* packed, int64_t ns, int M, int kind,
                               float scale, double* partial, cudaStream_t st);
+
+// Joint-space RBF baseline ("Fastron RBF"): joint vectors as zero-padded pseudo points.
+int joint_points(int D);
+cudaError_t launch_joint_points(const float* x, int64_t n, int64_t ldx, int D, float4* out, cudaStream_t st);
+cudaError_t launch_score_joint(const float4* qpts, int64_t nq, const float* packed, int64_t ns, int D, int kind,
+                               float scale, float* score, int8_t* label, double* partial, cudaStream_t st);
+cudaError_t launch_gram_joint(const float* packed, int64_t n, int D, int kind, float* K, int64_t ldk, cudaStream_t st);
 
 // K3: Gram
 cudaError_t launch_gram(const float* packed, int64_t n, int M, int kind, float* K, int64_t ldk, cudaStream_t st);

@@ -46,7 +46,7 @@ int score_queries_per_cta(int M) { return kNT * qt_for(padded_m(M)); }
 // pack: spos float4 [M][lds] + alpha -> scaled, paired tiles
 // ---------------------------------------------------------------------------------
 __global__ void pack_kernel(const float4* __restrict__ spos, int64_t lds, const float* __restrict__ alpha, int64_t ns,
-                            int M, int MP, float scale, float* __restrict__ packed, int64_t n_slots) {
+                            int M, int MP, float scale, float pad, float* __restrict__ packed, int64_t n_slots) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_slots) return;
   const int64_t tile = i / kTileSupports;
@@ -61,7 +61,7 @@ __global__ void pack_kernel(const float4* __restrict__ spos, int64_t lds, const 
     if (live && m1 < M) b = spos[(int64_t)m1 * lds + i];
     float ax = __fmul_rn(a.x, scale), ay = __fmul_rn(a.y, scale), az = __fmul_rn(a.z, scale);
     float bx = __fmul_rn(b.x, scale), by = __fmul_rn(b.y, scale), bz = __fmul_rn(b.z, scale);
-    if (m1 >= M) bx = by = bz = kPadCoord;  // padded control point: term is exactly 0
+    if (m1 >= M) bx = by = bz = pad;  // padded control point: term exactly 0 (FK) / no distance (joint)
     reinterpret_cast<float4*>(rec + p * 8)[0] = make_float4(ax, bx, ay, by);
     reinterpret_cast<float4*>(rec + p * 8)[1] = make_float4(az, bz, 0.f, 0.f);
   }
@@ -69,12 +69,12 @@ __global__ void pack_kernel(const float4* __restrict__ spos, int64_t lds, const 
 }
 
 cudaError_t launch_pack(const float4* spos, int64_t lds, const float* alpha, int64_t ns, int M, float scale,
-                        float* packed, cudaStream_t st) {
+                        float* packed, cudaStream_t st, bool joint) {
   const int64_t slots = n_support_tiles(ns) * kTileSupports;
   if (slots == 0) return cudaSuccess;
   const int threads = 256;
-  pack_kernel<<<(unsigned)((slots + threads - 1) / threads), threads, 0, st>>>(spos, lds, alpha, ns, M, padded_m(M),
-                                                                                 scale, packed, slots);
+  pack_kernel<<<(unsigned)((slots + threads - 1) / threads), threads, 0, st>>>(
+      spos, lds, alpha, ns, M, padded_m(M), scale, joint ? 0.0f : kPadCoord, packed, slots);
   g_launches.fetch_add(1);
   return cudaGetLastError();
 }
@@ -82,7 +82,11 @@ cudaError_t launch_pack(const float4* spos, int64_t lds, const float* alpha, int
 // ---------------------------------------------------------------------------------
 // the scoring kernel (positions mode and fused edge mode)
 // ---------------------------------------------------------------------------------
-enum { MODE_POS = 0, MODE_EDGE = 1 };
+// MODE_POS: FK-kernel score of control-point positions (Eq. 4); MODE_EDGE: fused edge
+// rounds; MODE_JOINT: the joint-space RBF kernel of the paper's "Fastron RBF" baseline
+// (Table I): one RBF term of the whole joint-vector distance,
+// with the joint vector laid out as ceil(D/3) zero-padded pseudo "control points".
+enum { MODE_POS = 0, MODE_EDGE = 1, MODE_JOINT = 2 };
 
 struct ScoreArgs {
   const float4* qpos;
@@ -109,6 +113,7 @@ struct ScoreArgs {
   int32_t* next_count;
   uint8_t* in_collision;
   int32_t* hit_index;
+  double denom;  // M for the FK kernel's 1/M mean (Eq. 4), 1 for the joint-space kernel
 };
 
 // Position k of the visiting order of round r, lane l: evens first, then odds (R11).
@@ -189,7 +194,7 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
     float px[MP], py[MP], pz[MP];
 #pragma unroll
     for (int m = 0; m < MP; ++m) px[m] = py[m] = pz[m] = 0.0f;
-    if (MODE == MODE_POS) {
+    if (MODE == MODE_POS || MODE == MODE_JOINT) {
       if (vq < A.nq) {
 #pragma unroll
         for (int m = 0; m < MP; ++m) {
@@ -246,6 +251,37 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
 #pragma unroll 2
     for (int s = 0; s < kTileSupports; ++s) {
       const float* rec = T + s * NP * 8;
+      const double a = alpha[s];
+      if (MODE == MODE_JOINT) {
+        // joint-space RBF: accumulate the squared distance over all pseudo points, one MUFU
+        f2 s2[QT];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          const float4 xy = *reinterpret_cast<const float4*>(rec + p * 8);
+          const float2 zz = *reinterpret_cast<const float2*>(rec + p * 8 + 4);
+          const f2 vx = pk(xy.x, xy.y), vy = pk(xy.z, xy.w), vz = pk(zz.x, zz.y);
+#pragma unroll
+          for (int j = 0; j < QT; ++j) {
+            const f2 dx = sub2(ux[j][p], vx), dy = sub2(uy[j][p], vy), dz = sub2(uz[j][p], vz);
+            s2[j] = p == 0 ? mul2(dx, dx) : fma2(dx, dx, s2[j]);
+            s2[j] = fma2(dy, dy, s2[j]);
+            s2[j] = fma2(dz, dz, s2[j]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < QT; ++j) {
+          const float d2 = lo(s2[j]) + hi(s2[j]);
+          float t;
+          if (KIND == kGaussian) {
+            t = ex2_neg(d2);
+          } else {
+            const float w = 1.0f + d2;
+            t = rcp_approx(w * w);
+          }
+          f[j] = fma(a, nonneg_f32_to_f64(t), f[j]);
+        }
+        continue;
+      }
       f2 acc[QT];
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
@@ -275,7 +311,6 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
         }
 #endif
       }
-      const double a = alpha[s];
 #pragma unroll
       for (int j = 0; j < QT; ++j) {
 #if FASTRON_ACC_SPLIT
@@ -300,14 +335,14 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
     const int64_t vq = q_base + j * kNT + tid;
     if (A.n_splits > 1) {
       if (vq < nq_live) A.partial[(int64_t)split * A.nq + vq] = f[j];
-    } else if (MODE == MODE_POS) {
+    } else if (MODE == MODE_POS || MODE == MODE_JOINT) {
       if (vq < A.nq) {
-        const double fm = f[j] / (double)A.M;
+        const double fm = f[j] / A.denom;
         if (A.score) A.score[vq] = (float)fm;
         if (A.label) A.label[vq] = fm > 0.0 ? 1 : -1;
       }
     } else {
-      edge_vote(A, vq, f[j] / (double)A.M);
+      edge_vote(A, vq, f[j] / A.denom);
     }
   }
 }
@@ -325,8 +360,8 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ S
   double f = 0.0;
   if (vq < nq_live)
     for (int s = 0; s < A.n_splits; ++s) f += A.partial[(int64_t)s * A.nq + vq];
-  const double fm = f / (double)A.M;
-  if (MODE == MODE_POS) {
+  const double fm = f / A.denom;
+  if (MODE == MODE_POS || MODE == MODE_JOINT) {
     if (A.score) A.score[vq] = (float)fm;
     if (A.label) A.label[vq] = fm > 0.0 ? 1 : -1;
   } else {
@@ -440,6 +475,59 @@ static cudaError_t dispatch(const ScoreArgs& A, const FkParams& P, int64_t nq, i
 #undef FASTRON_CASE
 }
 
+// joint vectors [n][ldx] (D dims) -> pseudo points float4 [ceil(D/3)][n], zero padded
+__global__ void joint_points_kernel(const float* __restrict__ x, int64_t n, int64_t ldx, int D, float4* __restrict__ out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const float* xk = x + k * ldx;
+  const int Mj = (D + 2) / 3;
+  for (int m = 0; m < Mj; ++m) {
+    const int d = 3 * m;
+    out[(int64_t)m * n + k] = make_float4(__ldg(xk + d), d + 1 < D ? __ldg(xk + d + 1) : 0.0f,
+                                          d + 2 < D ? __ldg(xk + d + 2) : 0.0f, 0.0f);
+  }
+}
+
+int joint_points(int D) { return (D + 2) / 3; }
+
+cudaError_t launch_joint_points(const float* x, int64_t n, int64_t ldx, int D, float4* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  joint_points_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, n, ldx, D, out);
+  g_launches.fetch_add(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_score_joint(const float4* qpts, int64_t nq, const float* packed, int64_t ns, int D, int kind,
+                               float scale, float* score, int8_t* label, double* partial, cudaStream_t st) {
+  if (nq <= 0) return cudaSuccess;
+  ScoreArgs A = {};
+  A.qpos = qpts;
+  A.ldq = nq;
+  A.nq = nq;
+  A.packed = packed;
+  A.M = joint_points(D);
+  A.scale = scale;
+  A.score = score;
+  A.label = label;
+  A.partial = partial;
+  A.denom = 1.0;
+  FkParams P = {};
+  const int MP = padded_m(A.M);
+  switch (MP) {
+    case 2:
+      return kind == kGaussian ? run_score<2, kGaussian, MODE_JOINT>(A, P, nq, ns, st)
+                               : run_score<2, kRQ, MODE_JOINT>(A, P, nq, ns, st);
+    case 4:
+      return kind == kGaussian ? run_score<4, kGaussian, MODE_JOINT>(A, P, nq, ns, st)
+                               : run_score<4, kRQ, MODE_JOINT>(A, P, nq, ns, st);
+    case 6:
+      return kind == kGaussian ? run_score<6, kGaussian, MODE_JOINT>(A, P, nq, ns, st)
+                               : run_score<6, kRQ, MODE_JOINT>(A, P, nq, ns, st);
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
 ScorePlan plan_score(int64_t nq, int64_t ns, int M, int kind) {
   (void)kind;
   return make_plan(nq, ns, M, 3);
@@ -458,6 +546,7 @@ cudaError_t launch_score(const float4* qpos, int64_t nq, int64_t ldq, const floa
   A.score = score;
   A.label = label;
   A.partial = partial;
+  A.denom = (double)M;
   FkParams P = {};
   return dispatch<MODE_POS>(A, P, nq, ns, kind, st);
 }
@@ -482,6 +571,7 @@ cudaError_t launch_edge_round(const FkParams& P, const EdgeRound& R, const float
   A.next_count = R.next_count;
   A.in_collision = R.in_collision;
   A.hit_index = R.hit_index;
+  A.denom = (double)M;
   return dispatch<MODE_EDGE>(A, P, A.nq, ns, kind, st);
 }
 

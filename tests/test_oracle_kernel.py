@@ -144,3 +144,32 @@ def test_coincident_control_points_still_pd():
     K = oracle.gram(oracle.RQ, 2.0, pos)
     assert np.linalg.matrix_rank(K1, tol=1e-10) < 4
     assert np.linalg.eigvalsh(K)[0] > 1e-6
+
+
+# ---- joint-space RBF ("Fastron RBF" baseline, Table I) ----
+
+def test_joint_kernel_worked_values():
+    """Eq. 3 on raw joint vectors: ||x - x'||^2 = 1 with gamma = 2 -> (1 + 1)^-2 = 0.25
+    (SPEC.md:130); Gaussian gamma = ln 2 -> 0.5; identical vectors -> 1."""
+    x = np.zeros(7, np.float32)
+    xp = np.zeros(7, np.float32)
+    xp[3] = 1.0
+    assert oracle.joint_kernel(oracle.RQ, 2.0, x, xp) == 0.25
+    assert oracle.joint_kernel(oracle.GAUSSIAN, math.log(2), x, xp) == pytest.approx(0.5, rel=1e-15)
+    xp2 = np.array([0.5, 0.5, 0.5, 0.5, 0, 0, 0], np.float32)  # squared distance 1
+    assert oracle.joint_kernel(oracle.RQ, 2.0, x, xp2) == 0.25
+    assert oracle.joint_kernel(oracle.RQ, 5.0, xp2, xp2) == 1.0
+
+
+def test_joint_score_and_gram_properties():
+    """Brute force on a tiny input, symmetry, unit diagonal and PD (the RQ kernel is PD,
+    PAPER.md:123)."""
+    rng = np.random.default_rng(3)
+    X = rng.uniform(-np.pi, np.pi, size=(40, 7)).astype(np.float32)
+    a = rng.standard_normal(40).astype(np.float32)
+    K = oracle.gram_joint(oracle.RQ, 1.0, X)
+    assert np.array_equal(K, K.T) and np.all(np.diag(K) == 1.0)
+    assert np.linalg.eigvalsh(K)[0] > 1e-10 * np.linalg.eigvalsh(K)[-1]
+    f, lab = oracle.score_joint(oracle.RQ, 1.0, X[:5], X, a)
+    np.testing.assert_allclose(f, K[:5] @ a.astype(np.float64), rtol=1e-12, atol=1e-13)
+    assert np.array_equal(lab, np.where(f > 0, 1, -1))
