@@ -234,6 +234,19 @@ def _time_rows(fb, torch, kind):
     res = fb.train_result(out["result"])
     rows["cfg3_train"] = {"ms": ms, **res, "us_per_iteration": ms * 1e3 / max(res["iterations"], 1),
                           "positive_fraction": float((y > 0).float().mean().item())}
+    # the same Algorithm 1 with lazily computed, cached K columns (no Gram)
+    lz = {}
+    lws = torch.empty(fb.load_library().fastron_train_lazy_workspace_bytes(len(tw.X), 8, 4096), dtype=torch.uint8,
+                      device="cuda")
+
+    def train_lazy():
+        lz.update(fb.fastron_train_lazy(pos, y, tw.kind, tw.gamma, tw.beta, tw.iter_max, cache_cols=4096,
+                                        workspace=lws))
+
+    ms = timed(train_lazy, 3)
+    resl = fb.train_result(lz["result"])
+    rows["cfg3_train_lazy"] = {"ms": ms, **resl, "us_per_iteration": ms * 1e3 / max(resl["iterations"], 1),
+                               "same_as_full_gram": resl == res}
     # cfg5: M = 16 scoring (1M of the 10M queries x 20k supports) and the 20k x 20k Gram rebuild (R21)
     wl = W.score_workload("cfg5", n_queries=1_000_000)
     spos = fb.fastron_fk(wl.robot, torch.from_numpy(wl.supports).cuda())

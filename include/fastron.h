@@ -174,6 +174,29 @@ fastron_status fastron_train(const float* K, int64_t n, int64_t ldk, const int8_
                              int32_t* trace, fastron_train_result* result, void* stream);
 
 /*
+ * fastron_train_lazy — Algorithm 1 with lazy kernel-matrix columns ("a column
+ * of K can be computed and stored only when needed", :225 computeKernelMatrixColumn):
+ * no Gram matrix is formed. The column of the selected index is computed inside the
+ * persistent cluster kernel from the pre-scaled training points (held in shared memory)
+ * and stored in a column cache of cache_cols columns; later steps on the same index
+ * read it back. Columns are bit-identical to fastron_gram's, so the result equals
+ * fastron_train(fastron_gram(pos)) exactly.
+ *   pos: device float4 [n_cp][ldp] control points of the n training configurations;
+ *   k: the FK-kernel term (n_cp in {1..4, 7, 8, 15, 16}: padded to 4, 8 or 16);
+ *   y, beta, iter_max, s_max, alpha_inout, F_inout, support_idx, trace, result: as
+ *   fastron_train. cache_cols >= 0 (columns beyond the cache are recomputed).
+ *   workspace: >= fastron_train_lazy_workspace_bytes(n, n_cp, cache_cols).
+ * n <= fastron_train_lazy_max_n(n_cp), else FASTRON_ERR_UNSUPPORTED.
+ */
+int64_t fastron_train_lazy_max_n(int32_t n_cp);
+size_t fastron_train_lazy_workspace_bytes(int64_t n, int32_t n_cp, int64_t cache_cols);
+fastron_status fastron_train_lazy(const float* pos, int64_t n, int64_t ldp, int32_t n_cp, fastron_kernel k,
+                                  const int8_t* y, double beta, int64_t iter_max, int64_t s_max,
+                                  double* alpha_inout, double* F_inout, int32_t* support_idx, int32_t* trace,
+                                  fastron_train_result* result, int64_t cache_cols, void* workspace,
+                                  size_t workspace_bytes, void* stream);
+
+/*
  * fastron_edge_check — discrete motion-planning edge check (BASELINE.json cfg4,
  * SPEC.md:379-387, R11): for edge e and k = 0..n_interp-1,
  * q_k = qa + t_k (qb - qa) with t_k = k / (n_interp - 1) in fp32 (t = 0 if n_interp = 1),

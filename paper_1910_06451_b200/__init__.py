@@ -30,7 +30,8 @@ EXPORTED = [
     "fastron_query_workspace_bytes", "fastron_query", "fastron_last_error", "fastron_version",
     "fastron_launch_count", "fastron_model_bytes", "fastron_model_pack", "fastron_score_packed_workspace_bytes",
     "fastron_score_packed", "fastron_score_joint_workspace_bytes", "fastron_score_joint",
-    "fastron_gram_joint_workspace_bytes", "fastron_gram_joint",
+    "fastron_gram_joint_workspace_bytes", "fastron_gram_joint", "fastron_train_lazy_max_n",
+    "fastron_train_lazy_workspace_bytes", "fastron_train_lazy",
 ]
 
 
@@ -91,6 +92,12 @@ def load_library(path: str = LIB_PATH):
     L.fastron_gram_joint_workspace_bytes.argtypes = [i64, i32]
     L.fastron_gram_joint_workspace_bytes.restype = sz
     L.fastron_gram_joint.argtypes = [vp, i64, i64, i32, fastron_kernel, vp, i64, vp, sz, vp]
+    L.fastron_train_lazy_max_n.argtypes = [i32]
+    L.fastron_train_lazy_max_n.restype = i64
+    L.fastron_train_lazy_workspace_bytes.argtypes = [i64, i32, i64]
+    L.fastron_train_lazy_workspace_bytes.restype = sz
+    L.fastron_train_lazy.argtypes = [vp, i64, i64, i32, fastron_kernel, vp, ctypes.c_double, i64, i64, vp, vp, vp, vp,
+                                     vp, i64, vp, sz, vp]
     L.fastron_gram_workspace_bytes.argtypes = [i64, i32]
     L.fastron_gram_workspace_bytes.restype = sz
     L.fastron_gram.argtypes = [vp, i64, i64, i32, fastron_kernel, vp, i64, vp, sz, vp]
@@ -104,7 +111,7 @@ def load_library(path: str = LIB_PATH):
     L.fastron_query_workspace_bytes.restype = sz
     L.fastron_query.argtypes = [rp, vp, i64, i64, vp, vp, i64, i64, fastron_kernel, vp, vp, vp, sz, vp]
     for f in ("fastron_fk", "fastron_score", "fastron_gram", "fastron_train", "fastron_edge_check", "fastron_query",
-              "fastron_model_pack", "fastron_score_packed", "fastron_score_joint", "fastron_gram_joint"):
+              "fastron_model_pack", "fastron_score_packed", "fastron_score_joint", "fastron_gram_joint", "fastron_train_lazy"):
         getattr(L, f).restype = st
     L.fastron_last_error.argtypes = []
     L.fastron_last_error.restype = ctypes.c_char_p
@@ -319,6 +326,35 @@ def fastron_train(K, y, beta: float = 1.0, iter_max: int = 20000, s_max: Optiona
     _check(L.fastron_train(_ptr(K), n, K.stride(0) if n else 1, _ptr(y), float(beta), int(iter_max), s_max,
                            _ptr(alpha), _ptr(F), _ptr(sup) if sup is not None and sup is not False else None,
                            _ptr(tr) if tr is not None and tr is not False else None, _ptr(res), _stream(stream)))
+    return dict(alpha=alpha, F=F, support_idx=sup, trace=tr, result=res)
+
+
+def fastron_train_lazy(pos, y, kind: int, gamma: float, beta: float = 1.0, iter_max: int = 20000,
+                       s_max: Optional[int] = None, alpha=None, F=None, cache_cols: Optional[int] = None,
+                       support_idx=True, trace=True, result=None, workspace=None, stream=None):
+    """Algorithm 1 with lazily computed, cached K columns (no Gram). pos: (M, n, 4) control points."""
+    import torch
+    L = load_library()
+    _require_cuda(pos, y, alpha, F)
+    M, n = pos.shape[0], pos.shape[1]
+    dev = pos.device
+    s_max = n if s_max is None else int(s_max)
+    cache_cols = min(n, 4096) if cache_cols is None else int(cache_cols)
+    if alpha is None:
+        alpha = torch.zeros(n, dtype=torch.float64, device=dev)
+    if F is None:
+        F = torch.zeros(n, dtype=torch.float64, device=dev)
+    sup = torch.empty(max(n, 1), dtype=torch.int32, device=dev) if support_idx is True else support_idx
+    tr = torch.empty(max(iter_max, 1), dtype=torch.int32, device=dev) if trace is True else trace
+    res = torch.zeros(ctypes.sizeof(fastron_train_result), dtype=torch.uint8, device=dev) if result is None else result
+    need = L.fastron_train_lazy_workspace_bytes(n, M, cache_cols)
+    if workspace is None or workspace.numel() < need:
+        workspace = _workspace(need, dev)
+    _check(L.fastron_train_lazy(_ptr(pos), n, pos.stride(0) // 4, M, _kernel(kind, gamma), _ptr(y), float(beta),
+                                int(iter_max), s_max, _ptr(alpha), _ptr(F),
+                                _ptr(sup) if sup is not None and sup is not False else None,
+                                _ptr(tr) if tr is not None and tr is not False else None, _ptr(res), cache_cols,
+                                _ptr(workspace), workspace.numel(), _stream(stream)))
     return dict(alpha=alpha, F=F, support_idx=sup, trace=tr, result=res)
 
 

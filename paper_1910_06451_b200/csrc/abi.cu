@@ -311,6 +311,50 @@ fastron_status fastron_train(const float* K, int64_t n, int64_t ldk, const int8_
                      "fastron_train");
 }
 
+int64_t fastron_train_lazy_max_n(int32_t n_cp) {
+  if (n_cp < 1 || n_cp > 16) return 0;
+  return train_lazy_max_n(n_cp);
+}
+
+size_t fastron_train_lazy_workspace_bytes(int64_t n, int32_t n_cp, int64_t cache_cols) {
+  if (n < 0 || n_cp < 1 || n_cp > FASTRON_MAX_CP || cache_cols < 0) return 0;
+  return align_up(packed_bytes(n, n_cp)) + align_up((size_t)cache_cols * (size_t)n * 4);
+}
+
+fastron_status fastron_train_lazy(const float* pos, int64_t n, int64_t ldp, int32_t n_cp, fastron_kernel k,
+                                  const int8_t* y, double beta, int64_t iter_max, int64_t s_max,
+                                  double* alpha_inout, double* F_inout, int32_t* support_idx, int32_t* trace,
+                                  fastron_train_result* result, int64_t cache_cols, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+  fastron_status s = check_kernel(k);
+  if (s != FASTRON_OK) return s;
+  FASTRON_REQUIRE(n >= 0 && iter_max >= 0 && s_max >= 0 && cache_cols >= 0, "sizes must be >= 0");
+  FASTRON_REQUIRE(n_cp >= 1 && n_cp <= FASTRON_MAX_CP, "n_cp must be in [1,32], got %d", n_cp);
+  FASTRON_REQUIRE(std::isfinite(beta) && beta >= 1.0, "beta must be >= 1 (PAPER.md:189), got %g", beta);
+  FASTRON_REQUIRE(result != nullptr, "result is NULL");
+  if (n_cp > 16) return fail(FASTRON_ERR_UNSUPPORTED, "fastron_train_lazy supports n_cp <= 16, got %d", n_cp);
+  if (n > fastron_train_lazy_max_n(n_cp))
+    return fail(FASTRON_ERR_UNSUPPORTED, "n = %lld exceeds fastron_train_lazy_max_n = %lld", (long long)n,
+                (long long)fastron_train_lazy_max_n(n_cp));
+  if (n == 0) return cuda_status(cudaMemsetAsync(result, 0, sizeof(*result), S(stream)), "fastron_train_lazy");
+  FASTRON_REQUIRE(pos && y && alpha_inout && F_inout, "pos, y, alpha_inout and F_inout must be non-NULL");
+  FASTRON_REQUIRE(ldp >= n, "ldp (%lld) < n (%lld)", (long long)ldp, (long long)n);
+  const size_t need = fastron_train_lazy_workspace_bytes(n, n_cp, cache_cols);
+  if (workspace_bytes < need || !workspace)
+    return fail(FASTRON_ERR_WORKSPACE, "fastron_train_lazy needs %zu workspace bytes, got %zu", need, workspace_bytes);
+  FASTRON_REQUIRE(((uintptr_t)workspace & 255) == 0, "workspace must be 256-byte aligned");
+  char* ws = static_cast<char*>(workspace);
+  float* packed = reinterpret_cast<float*>(ws);
+  float* cache = reinterpret_cast<float*>(ws + align_up(packed_bytes(n, n_cp)));
+  cudaStream_t st = S(stream);
+  cudaError_t e =
+      launch_pack(reinterpret_cast<const float4*>(pos), ldp, nullptr, n, n_cp, kernel_scale(k), packed, st);
+  if (e == cudaSuccess)
+    e = launch_train_lazy(packed, n, n_cp, k.kind, y, beta, iter_max, s_max, alpha_inout, F_inout, support_idx, trace,
+                          result, cache, cache_cols, st);
+  return cuda_status(e, "fastron_train_lazy");
+}
+
 size_t fastron_edge_workspace_bytes(int64_t n_edges, int64_t ns, int32_t n_cp) {
   if (n_edges < 0 || ns < 0 || n_cp < 1 || n_cp > FASTRON_MAX_CP) return 0;
   const size_t lists = 2 * align_up((size_t)n_edges * 4) + 256;  // two active lists + two counters

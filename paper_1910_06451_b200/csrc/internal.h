@@ -79,5 +79,9 @@ int64_t train_max_n();
 cudaError_t launch_train(const float* K, int64_t n, int64_t ldk, const int8_t* y, double beta, int64_t iter_max,
                          int64_t s_max, double* alpha, double* F, int32_t* support_idx, int32_t* trace, void* result,
                          cudaStream_t st);
+int64_t train_lazy_max_n(int M);
+cudaError_t launch_train_lazy(const float* packed, int64_t n, int M, int kind, const int8_t* y, double beta,
+                              int64_t iter_max, int64_t s_max, double* alpha, double* F, int32_t* support_idx,
+                              int32_t* trace, void* result, float* cache, int64_t cache_cols, cudaStream_t st);
 
 }  // namespace fastron

@@ -51,17 +51,21 @@ struct TrainResultDev {
   int32_t converged, n_support;
 };
 
-struct Cand {    // a (key, index) winner with its payload
-  uint64_t key;  // order-preserving bits of the value (-0 == +0)
-  double G;      // y F at the winner (min pass)
-  double Y;      // y alpha at the winner
-  int32_t idx;   // kNone if empty
-  int32_t y;     // label at the winner
+struct Cand {     // a (key, index) winner with its payload
+  uint64_t key;   // order-preserving bits of the value (-0 == +0)
+  double G;       // y F at the winner (min pass)
+  double Y;       // y alpha at the winner
+  int32_t idx;    // kNone if empty
+  int32_t y;      // label at the winner
+  int32_t slot;   // lazy mode: column-cache slot of the winner's K column (-1: not cached)
+  int32_t pad;
 };
 
 struct Decision {
   int32_t action;
   int32_t idx;    // row of the rank-one update = slot whose Y changes
+  int32_t slot;      // lazy mode: cache slot holding column idx (-1: compute it)
+  int32_t new_slot;  // lazy mode: cache slot to store the computed column in (-1: none)
   double delta;   // Eq. 6 (or -alpha_i for a removal)
   double newY;    // y_i alpha_i after the step
   int64_t nnz;    // count(alpha != 0) after the step
@@ -81,9 +85,15 @@ struct TrainArgs {
   int32_t* trace;
   TrainResultDev* result;
   int64_t chunk;
+  // lazy-column mode: K columns computed on demand and cached
+  const float* packed;   // pre-scaled training points in the scoring tile layout
+  float* cache;          // [cache_cols][n]
+  int64_t cache_cols;
+  int32_t M, m_pow2;
+  float inv_m;
 };
 
-__device__ __forceinline__ Cand cand_none(bool for_max) { return Cand{for_max ? 0ull : ~0ull, 0.0, 0.0, kNone, 1}; }
+__device__ __forceinline__ Cand cand_none(bool for_max) { return Cand{for_max ? 0ull : ~0ull, 0.0, 0.0, kNone, 1, -1, 0}; }
 
 // Monotone map double -> uint64 (a < b  <=>  key(a) < key(b) for non-NaN; -0 == +0).
 __device__ __forceinline__ uint64_t order_key(double x) {
@@ -126,6 +136,8 @@ __device__ __forceinline__ Cand warp_best(const Cand& c) {
   b.G = __shfl_sync(0xffffffffu, c.G, src);
   b.Y = __shfl_sync(0xffffffffu, c.Y, src);
   b.y = __shfl_sync(0xffffffffu, c.y, src);
+  b.slot = __shfl_sync(0xffffffffu, c.slot, src);
+  b.pad = 0;
   return b;
 }
 
@@ -135,9 +147,18 @@ __device__ __forceinline__ float ld_evict_last(const float* p, uint64_t pol) {
   return v;
 }
 
+// Lazy mode: column idx is read from its cache slot, or computed and stored in the next
+// free slot while the cache has room (computeKernelMatrixColumn).
+__device__ __forceinline__ void assign_column(Decision& d, int slot, int nfree, const TrainArgs& A) {
+  d.slot = slot;
+  d.new_slot = (slot < 0 && nfree < A.cache_cols) ? nfree : -1;
+}
+
 // Alg. 1's branch on the min candidate.
-__device__ __forceinline__ Decision decide_min(const Cand& b, int64_t iters, int64_t nnz, const TrainArgs& A) {
+__device__ __forceinline__ Decision decide_min(const Cand& b, int64_t iters, int64_t nnz, int nfree,
+                                               const TrainArgs& A) {
   Decision d = {};
+  d.slot = d.new_slot = -1;
   const bool has = b.idx != kNone;
   const double m = has ? key_value(b.key) : INFINITY;
   d.nnz = nnz;
@@ -152,6 +173,7 @@ __device__ __forceinline__ Decision decide_min(const Cand& b, int64_t iters, int
     d.delta = b.y > 0 ? sdelta : -sdelta;
     d.newY = __dadd_rn(b.Y, sdelta);                 // y_i (alpha_i + delta) (Eq. 7)
     d.nnz = nnz + (b.Y == 0.0 && d.newY != 0.0) - (b.Y != 0.0 && d.newY == 0.0);
+    assign_column(d, b.slot, nfree, A);
   } else {
     d.action = ACT_CHECK_REMOVAL;
     d.converged = m > 0.0;
@@ -160,21 +182,27 @@ __device__ __forceinline__ Decision decide_min(const Cand& b, int64_t iters, int
 }
 
 // Alg. 1's redundant-support branch.
-__device__ __forceinline__ Decision decide_removal(Decision d, const Cand& b) {
+__device__ __forceinline__ Decision decide_removal(Decision d, const Cand& b, int nfree, const TrainArgs& A) {
   if (b.idx != kNone && key_value(b.key) > 0.0) {
     d.action = ACT_REMOVE;
     d.idx = b.idx;
     d.delta = b.y > 0 ? -b.Y : b.Y;  // -alpha_i = -y_i (y_i alpha_i)
     d.newY = 0.0;
     d.nnz = d.nnz - 1;
+    assign_column(d, b.slot, nfree, A);
   } else {
     d.action = ACT_STOP;
   }
   return d;
 }
 
-template <int EPT>
+// LMP = 0: K is given (fastron_train). LMP > 0: lazy columns of the FK kernel with LMP
+// padded control points and term LKIND (fastron_train_lazy).
+template <int EPT, int LMP, int LKIND>
 __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constant__ TrainArgs A) {
+  constexpr bool LAZY = LMP > 0;
+  constexpr int LNP = LAZY ? LMP / 2 : 1;
+  constexpr int64_t LTF = tile_floats(LAZY ? LMP : 2);
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int C = (int)cluster.num_blocks();
@@ -182,6 +210,10 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* s_Y = reinterpret_cast<double*>(smem_raw);  // [chunk], owner-thread access only
+  // lazy mode: the slice's pre-scaled points (records of the scoring tile layout) and the
+  // cache slot of each local index's K column (owner-thread access only)
+  float* s_rec = reinterpret_cast<float*>(smem_raw + ((A.chunk * 8 + 15) & ~15ll));
+  int32_t* s_slot = reinterpret_cast<int32_t*>(s_rec + (LAZY ? A.chunk * LNP * 8 : 0));
   __shared__ Cand s_warp[2][kTrainWarps];
   __shared__ Cand s_cta[2];
   __shared__ int32_t s_cta_cnt[2];
@@ -211,6 +243,13 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
     if (live) s_Y[j] = neg ? -a : a;
     if (neg) yneg |= 1u << k;
     cnt0 += (live && a != 0.0);
+    if (LAZY && live) {
+      s_slot[j] = -1;
+      const int64_t g = lo + j;
+      const float4* src = reinterpret_cast<const float4*>(A.packed + (g / kTileSupports) * LTF + (g % kTileSupports) * LNP * 8);
+      float4* dst = reinterpret_cast<float4*>(s_rec + (int64_t)j * LNP * 8);
+      for (int w = 0; w < LNP * 2; ++w) dst[w] = src[w];
+    }
   }
   // initial count(alpha != 0) over the cluster
   {
@@ -240,6 +279,8 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
   int64_t iters = 0, n_add = 0, n_remove = 0;
   int upd_i = -1;  // row of the pending rank-one update of F
   double upd_delta = 0.0;
+  int upd_slot = -1, upd_new_slot = -1;  // lazy mode: where column upd_i comes from / goes to
+  int nfree = 0;                         // lazy mode: next free cache slot (uniform)
   int parity = 0;
   int converged = 0;
 
@@ -248,9 +289,41 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
     float kr[EPT];
     const bool have_upd = upd_i >= 0;
     if (have_upd) {
-      const float* Krow = A.K + (int64_t)upd_i * A.ldk + lo;
+      if (!LAZY || upd_slot >= 0) {
+        const float* Krow = LAZY ? A.cache + (int64_t)upd_slot * A.n + lo : A.K + (int64_t)upd_i * A.ldk + lo;
 #pragma unroll
-      for (int k = 0; k < EPT; ++k) kr[k] = ld_evict_last(Krow + koff[k], pol);
+        for (int k = 0; k < EPT; ++k) kr[k] = ld_evict_last(Krow + koff[k], pol);
+      } else if (LAZY) {
+        // computeKernelMatrixColumn(i): K(X_j, X_i) for the thread's slots,
+        // with the same term function and summation order as fastron_gram (bit-identical)
+        const float* wr = A.packed + (int64_t)(upd_i / kTileSupports) * LTF + (upd_i % kTileSupports) * LNP * 8;
+        f2 vx[LNP], vy[LNP], vz[LNP];
+#pragma unroll
+        for (int p = 0; p < LNP; ++p) {
+          const float4 xy = __ldg(reinterpret_cast<const float4*>(wr + p * 8));
+          const float2 zz = __ldg(reinterpret_cast<const float2*>(wr + p * 8 + 4));
+          vx[p] = pk(xy.x, xy.y);
+          vy[p] = pk(xy.z, xy.w);
+          vz[p] = pk(zz.x, zz.y);
+        }
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+          const float* rec = s_rec + (int64_t)koff[k] * LNP * 8;
+          f2 acc;
+#pragma unroll
+          for (int p = 0; p < LNP; ++p) {
+            const float4 xy = *reinterpret_cast<const float4*>(rec + p * 8);
+            const float2 zz = *reinterpret_cast<const float2*>(rec + p * 8 + 4);
+            const f2 t = term_pair<LKIND>(pk(xy.x, xy.y), pk(xy.z, xy.w), pk(zz.x, zz.y), vx[p], vy[p], vz[p]);
+            acc = p == 0 ? t : add2(acc, t);
+          }
+          const float ks = pair_sum(acc);
+          const float v = A.m_pow2 ? ks * A.inv_m : __fdiv_rn(ks, (float)A.M);
+          kr[k] = v;
+          const int j = k * kTrainNT + tid;
+          if (upd_new_slot >= 0 && j < len) A.cache[(int64_t)upd_new_slot * A.n + lo + j] = v;
+        }
+      }
     }
     double m0 = INFINITY, m1 = INFINITY;  // two interleaved chains (even / odd k)
     int k0 = -1, k1 = -1;
@@ -277,7 +350,8 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
       int widx;
       const int wl = warp_argbest<false>(order_key(mk), my_idx, wkey, widx);
       if (lane == wl) {  // the owner lane attaches the payload of the warp winner
-        s_warp[parity][warp] = Cand{wkey, mk, s_Y[mkk * kTrainNT + tid], widx, ((yneg >> mkk) & 1u) ? -1 : 1};
+        const int jw = mkk * kTrainNT + tid;
+        s_warp[parity][warp] = Cand{wkey, mk, s_Y[jw], widx, ((yneg >> mkk) & 1u) ? -1 : 1, LAZY ? s_slot[jw] : -1, 0};
       } else if (wl < 0 && lane == 0) {
         s_warp[parity][warp] = cand_none(false);
       }
@@ -288,7 +362,7 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
     if (warp == 0) {
       const Cand best = warp_best<false>(lane < kTrainWarps ? s_warp[parity][lane] : cand_none(false));
       if (C == 1) {
-        if (lane == 0) s_dec[parity] = decide_min(best, iters, nnz, A);
+        if (lane == 0) s_dec[parity] = decide_min(best, iters, nnz, nfree, A);
       } else if (lane == 0) {
         s_cta[parity] = best;
       }
@@ -297,7 +371,7 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
       cluster.sync();
       if (warp == 0) {
         const Cand best = warp_best<false>(lane < C ? *cluster.map_shared_rank(&s_cta[parity], lane) : cand_none(false));
-        if (lane == 0) s_dec[parity] = decide_min(best, iters, nnz, A);
+        if (lane == 0) s_dec[parity] = decide_min(best, iters, nnz, nfree, A);
       }
     }
     __syncthreads();
@@ -323,7 +397,8 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
         int widx;
         const int wl = warp_argbest<true>(order_key(rk), ridx, wkey, widx);
         if (lane == wl) {
-          s_warp[q][warp] = Cand{wkey, 0.0, s_Y[rkk * kTrainNT + tid], widx, ((yneg >> rkk) & 1u) ? -1 : 1};
+          const int jw = rkk * kTrainNT + tid;
+          s_warp[q][warp] = Cand{wkey, 0.0, s_Y[jw], widx, ((yneg >> rkk) & 1u) ? -1 : 1, LAZY ? s_slot[jw] : -1, 0};
         } else if (wl < 0 && lane == 0) {
           s_warp[q][warp] = cand_none(true);
         }
@@ -332,7 +407,7 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
       if (warp == 0) {
         const Cand best = warp_best<true>(lane < kTrainWarps ? s_warp[q][lane] : cand_none(true));
         if (C == 1) {
-          if (lane == 0) s_dec[q] = decide_removal(d, best);
+          if (lane == 0) s_dec[q] = decide_removal(d, best, nfree, A);
         } else if (lane == 0) {
           s_cta[q] = best;
         }
@@ -341,7 +416,7 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
         cluster.sync();
         if (warp == 0) {
           const Cand best = warp_best<true>(lane < C ? *cluster.map_shared_rank(&s_cta[q], lane) : cand_none(true));
-          if (lane == 0) s_dec[q] = decide_removal(d, best);
+          if (lane == 0) s_dec[q] = decide_removal(d, best, nfree, A);
         }
       }
       __syncthreads();
@@ -355,7 +430,15 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
     }
     // apply the step: the owner thread updates Y_i, everyone records the pending
     // rank-one update of G for the next pass
-    if (d.idx >= lo && d.idx < hi && ((d.idx - lo) % kTrainNT) == tid) s_Y[d.idx - lo] = d.newY;
+    if (d.idx >= lo && d.idx < hi && ((d.idx - lo) % kTrainNT) == tid) {
+      s_Y[d.idx - lo] = d.newY;
+      if (LAZY && d.new_slot >= 0) s_slot[d.idx - lo] = d.new_slot;
+    }
+    if (LAZY) {
+      upd_slot = d.slot;
+      upd_new_slot = d.new_slot;
+      if (d.new_slot >= 0) nfree = d.new_slot + 1;
+    }
     if (tid == 0 && rank == 0 && A.trace) A.trace[iters] = d.action == ACT_ADD ? d.idx : -(d.idx + 1);
     if (d.action == ACT_ADD) ++n_add;
     else ++n_remove;
@@ -427,18 +510,18 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
 
 int64_t train_max_n() { return kChunkMax * kMaxCluster; }
 
-template <int EPT>
-static cudaError_t launch_ept(const TrainArgs& A, int C, cudaStream_t st) {
+template <int EPT, int LMP = 0, int LKIND = 0>
+static cudaError_t launch_ept(const TrainArgs& A, int C, cudaStream_t st, size_t smem) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(train_kernel<EPT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(train_kernel<EPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kChunkMax * 8));
+    cudaFuncSetAttribute(train_kernel<EPT, LMP, LKIND>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(train_kernel<EPT, LMP, LKIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C, 1, 1);
   cfg.blockDim = dim3(kTrainNT, 1, 1);
-  cfg.dynamicSmemBytes = (size_t)A.chunk * 8;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
@@ -447,7 +530,7 @@ static cudaError_t launch_ept(const TrainArgs& A, int C, cudaStream_t st) {
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, train_kernel<EPT>, A);
+  return cudaLaunchKernelEx(&cfg, train_kernel<EPT, LMP, LKIND>, A);
 }
 
 cudaError_t launch_train(const float* K, int64_t n, int64_t ldk, const int8_t* y, double beta, int64_t iter_max,
@@ -475,12 +558,95 @@ cudaError_t launch_train(const float* K, int64_t n, int64_t ldk, const int8_t* y
   A.result = reinterpret_cast<TrainResultDev*>(result);
   A.chunk = (n + C - 1) / C;
   if (A.chunk < 1) A.chunk = 1;
+  A.packed = nullptr;
+  A.cache = nullptr;
+  A.cache_cols = 0;
+  A.M = 1;
+  A.m_pow2 = 1;
+  A.inv_m = 1.0f;
   const int64_t ept = (A.chunk + kTrainNT - 1) / kTrainNT;
+  const size_t smem = (size_t)A.chunk * 8;
   cudaError_t e;
-  if (ept <= 2) e = launch_ept<2>(A, C, st);
-  else if (ept <= 4) e = launch_ept<4>(A, C, st);
-  else if (ept <= 8) e = launch_ept<8>(A, C, st);
-  else e = launch_ept<12>(A, C, st);
+  if (ept <= 2) e = launch_ept<2>(A, C, st, smem);
+  else if (ept <= 4) e = launch_ept<4>(A, C, st, smem);
+  else if (ept <= 8) e = launch_ept<8>(A, C, st, smem);
+  else e = launch_ept<12>(A, C, st, smem);
+  g_launches.fetch_add(1);
+  return e;
+}
+
+// ---- lazy-column mode ----
+constexpr int64_t kLazySmem = 200 * 1024;  // shared-memory budget per CTA
+
+static int64_t lazy_bytes_per_slot(int MP) { return 8 + 4 + (int64_t)(MP / 2) * 32; }
+
+int64_t train_lazy_max_n(int M) {
+  const int MP = padded_m(M);
+  int64_t chunk = kLazySmem / lazy_bytes_per_slot(MP);
+  if (chunk > 4 * kTrainNT) chunk = 4 * kTrainNT;
+  return chunk * kMaxCluster;
+}
+
+template <int MP, int KIND>
+static cudaError_t launch_lazy_mp(const TrainArgs& A, int C, cudaStream_t st, size_t smem) {
+  const int64_t ept = (A.chunk + kTrainNT - 1) / kTrainNT;
+  if (ept <= 2) return launch_ept<2, MP, KIND>(A, C, st, smem);
+  return launch_ept<4, MP, KIND>(A, C, st, smem);
+}
+
+cudaError_t launch_train_lazy(const float* packed, int64_t n, int M, int kind, const int8_t* y, double beta,
+                              int64_t iter_max, int64_t s_max, double* alpha, double* F, int32_t* support_idx,
+                              int32_t* trace, void* result, float* cache, int64_t cache_cols, cudaStream_t st) {
+  const int MP = padded_m(M);
+  int64_t chunk_max = kLazySmem / lazy_bytes_per_slot(MP);
+  if (chunk_max > 4 * kTrainNT) chunk_max = 4 * kTrainNT;
+  int C = (int)((n + chunk_max - 1) / chunk_max);
+  if (C < 1) C = 1;
+  if (const char* env = getenv("FASTRON_TRAIN_CLUSTER")) {
+    const int c = atoi(env);
+    if (c > C) C = c;
+  }
+  if (C > kMaxCluster) return cudaErrorInvalidValue;
+  TrainArgs A;
+  A.K = nullptr;
+  A.n = n;
+  A.ldk = n;
+  A.y = y;
+  A.beta = beta;
+  A.iter_max = iter_max;
+  A.s_max = s_max;
+  A.alpha = alpha;
+  A.F = F;
+  A.support_idx = support_idx;
+  A.trace = trace;
+  A.result = reinterpret_cast<TrainResultDev*>(result);
+  A.chunk = (n + C - 1) / C;
+  if (A.chunk < 1) A.chunk = 1;
+  A.packed = packed;
+  A.cache = cache;
+  A.cache_cols = cache_cols;
+  A.M = M;
+  A.m_pow2 = (M & (M - 1)) == 0;
+  A.inv_m = 1.0f / (float)M;
+  const size_t smem = (size_t)((A.chunk * 8 + 15) & ~15ll) + (size_t)A.chunk * (MP / 2) * 32 + (size_t)A.chunk * 4;
+  cudaError_t e;
+  switch (MP) {
+#define FASTRON_LCASE(mp)                                                                              \
+  case mp:                                                                                             \
+    e = kind == kGaussian ? launch_lazy_mp<mp, kGaussian>(A, C, st, smem) : launch_lazy_mp<mp, kRQ>(A, C, st, smem); \
+    break;
+    FASTRON_LCASE(2)
+    FASTRON_LCASE(4)
+    FASTRON_LCASE(6)
+    FASTRON_LCASE(8)
+    FASTRON_LCASE(10)
+    FASTRON_LCASE(12)
+    FASTRON_LCASE(14)
+    FASTRON_LCASE(16)
+#undef FASTRON_LCASE
+    default:
+      return cudaErrorInvalidValue;
+  }
   g_launches.fetch_add(1);
   return e;
 }

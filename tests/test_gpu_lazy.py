@@ -1,0 +1,68 @@
+"""fastron_train_lazy (Algorithm 1 with lazily computed K columns)
+must reproduce fastron_train on the full Gram exactly: the columns are computed with the
+same term function, so the traces, alpha and F are bit-identical; and both match the
+oracle's Algorithm 1 on that Gram (R13)."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from gpu_helpers import dev, require_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+def _labels(robot, X, cubes, radius):
+    pos = oracle.fk(robot, X)
+    return W.capsule_aabb_labels(W.chain_points(pos[:, :8] if pos.shape[1] >= 8 else pos), cubes, radius)
+
+
+@pytest.mark.parametrize("n,m16,kind,cache,beta,s_max", [
+    (1000, False, 0, 4096, 1.0, None),
+    (5000, False, 0, 4096, 1.0, None),   # cfg3 itself (a 4-CTA cluster)
+    (1500, False, 1, 37, 2.0, None),     # tiny cache: most columns recomputed
+    (1200, True, 0, 0, 1.0, 100),        # M = 16, no cache at all, S_max gate
+])
+def test_lazy_equals_full_gram(n, m16, kind, cache, beta, s_max):
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    wl = W.train_workload(n)
+    robot = W.arm7(16) if m16 else wl.robot
+    y = W.capsule_aabb_labels(W.chain_points(oracle.fk(wl.robot, wl.X)), wl.cubes, wl.radius)
+    pos = fb.fastron_fk(robot, dev(wl.X))
+    K = fb.fastron_gram(pos, kind, wl.gamma)
+    yd = dev(y)
+    full = fb.fastron_train(K, yd, beta, 6000, s_max)
+    lazy = fb.fastron_train_lazy(pos, yd, kind, wl.gamma, beta, 6000, s_max, cache_cols=cache)
+    torch.cuda.synchronize()
+    rf, rl = fb.train_result(full["result"]), fb.train_result(lazy["result"])
+    assert rf == rl
+    it = rf["iterations"]
+    assert np.array_equal(full["trace"].cpu().numpy()[:it], lazy["trace"].cpu().numpy()[:it])
+    assert np.array_equal(full["alpha"].cpu().numpy(), lazy["alpha"].cpu().numpy())
+    assert np.array_equal(full["F"].cpu().numpy(), lazy["F"].cpu().numpy())
+    ns = rf["n_support"]
+    assert np.array_equal(full["support_idx"].cpu().numpy()[:ns], lazy["support_idx"].cpu().numpy()[:ns])
+    if n <= 1500:
+        r = oracle.train(K.cpu().numpy().astype(np.float64), y, beta, 6000, s_max)
+        assert r["iterations"] == it and np.array_equal(r["trace"], lazy["trace"].cpu().numpy()[:it])
+
+
+def test_lazy_warm_start():
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    wl = W.train_workload(900)
+    y = W.capsule_aabb_labels(W.chain_points(oracle.fk(wl.robot, wl.X)), wl.cubes, wl.radius)
+    pos = fb.fastron_fk(wl.robot, dev(wl.X))
+    K = fb.fastron_gram(pos, 0, wl.gamma)
+    first = oracle.train(K.cpu().numpy().astype(np.float64), y, 1.0, 200)
+    y2 = y.copy()
+    y2[::5] *= -1
+    a0, F0 = dev(first["alpha"], torch.float64), dev(first["F"], torch.float64)
+    lazy = fb.fastron_train_lazy(pos, dev(y2), 0, wl.gamma, 1.0, 3000, alpha=a0.clone(), F=F0.clone())
+    full = fb.fastron_train(K, dev(y2), 1.0, 3000, alpha=a0.clone(), F=F0.clone())
+    torch.cuda.synchronize()
+    assert fb.train_result(lazy["result"]) == fb.train_result(full["result"])
+    assert np.array_equal(lazy["alpha"].cpu().numpy(), full["alpha"].cpu().numpy())
