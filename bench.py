@@ -277,6 +277,34 @@ def _time_rows(fb, torch, kind):
                          "write_GBps": n5 * n5 * 4 / ms * 1e-6}
     del K5
     torch.cuda.empty_cache()
+    # the model-update cycle (Table I "update time" 55.8 ms incl. FCL labelling):
+    # fit on cfg3, move 3 of the 6 cubes by 0.1 m (R21), then 2 draws near every support point +
+    # 1,000 uniform draws, GPU capsule labelling, Gram, warm-started Algorithm 1
+    from paper_1910_06451_b200.model import CapsuleScene, FastronModel
+    chain = [-1, 0, 1, 2, 3, 4, 5, 6, 7]
+    mdl = FastronModel(tw.robot, tw.kind, tw.gamma, tw.beta, tw.iter_max)
+    mdl.fit(X, y)
+    ns0 = mdl.supports.shape[0]
+    rng = np.random.default_rng(11)
+    moved = tw.cubes.copy()
+    for j in rng.choice(len(moved), 3, replace=False):
+        v = rng.standard_normal(3)
+        moved[j] += 0.1 * v / np.linalg.norm(v)
+    scene = CapsuleScene(np.array(chain), moved, tw.radius)
+    z = torch.from_numpy(rng.standard_normal((2 * ns0, 7)).astype(np.float32)).cuda()
+    u = torch.from_numpy(rng.uniform(0, 1, (1000, 7)).astype(np.float32)).cuda()
+    sig = torch.full((7,), 0.05 * 2 * np.pi, device="cuda")
+    lo_t, hi_t = torch.full((7,), -np.pi, device="cuda"), torch.full((7,), np.pi, device="cuda")
+    snap = (mdl.supports.clone(), mdl.alpha.clone(), mdl.model)
+    upd = {}
+
+    def cycle():
+        mdl.supports, mdl.alpha, mdl.model = snap[0], snap[1], snap[2]
+        upd["res"] = mdl.update(scene, z, u, sig, lo_t, hi_t, 2)[0]
+
+    ms = timed(cycle, 3)
+    rows["cfg3_update_cycle"] = {"ms": ms, "n_dataset": 3 * ns0 + 1000, **upd["res"],
+                                 "paper_update_ms": 55.8, "note": "samples + FK + GPU labelling + Gram + warm-started Alg. 1"}
     # Table I context: Fastron FK (|S| = 303, M = 8) vs the joint-space "Fastron RBF" kernel
     # (|S| = 2369), the paper's mean support-set sizes, 1M queries each
     hw = W.score_workload("headline", n_queries=1_000_000)

@@ -128,6 +128,12 @@ fastron_status fastron_score(const float* qpos, int64_t nq, int64_t ldq, const f
  *   fastron_score_packed_workspace_bytes(nq, ns, n_cp) (may be 0 bytes).
  */
 size_t fastron_model_bytes(int64_t ns, int32_t n_cp);
+/* fastron_score_packed_f64: the same scores in fp64 (before the fp32 rounding), e.g. the
+ * margins F = K alpha a warm-started Algorithm 1 needs. score64: device
+ * double [nq]. */
+fastron_status fastron_score_packed_f64(const float* qpos, int64_t nq, int64_t ldq, const void* packed, int64_t ns,
+                                        int32_t n_cp, fastron_kernel k, double* score64, void* workspace,
+                                        size_t workspace_bytes, void* stream);
 fastron_status fastron_model_pack(const float* spos, const float* alpha, int64_t ns, int64_t lds, int32_t n_cp,
                                   fastron_kernel k, void* packed, size_t packed_bytes, void* stream);
 size_t fastron_score_packed_workspace_bytes(int64_t nq, int64_t ns, int32_t n_cp);
@@ -195,6 +201,31 @@ fastron_status fastron_train_lazy(const float* pos, int64_t n, int64_t ldp, int3
                                   double* alpha_inout, double* F_inout, int32_t* support_idx, int32_t* trace,
                                   fastron_train_result* result, int64_t cache_cols, void* workspace,
                                   size_t workspace_bytes, void* stream);
+
+/*
+ * Model-update cycle (PAPER.md:272, "two-stage active learning"; :219 loadPreviousModel).
+ *
+ * fastron_active_samples — stage 1: n_near samples around each of the ns support points,
+ *   clamp(S_i + sigma * z, lo, hi); stage 2: n_uniform samples lo + u (hi - lo). The random
+ *   numbers are inputs: z device float [ns*n_near][dof] ~ N(0,1), u device float
+ *   [n_uniform][dof] ~ U[0,1). sigma, lo, hi: device float [dof]. out: device float
+ *   [ns*n_near + n_uniform][ldo], stage-1 rows first (support-major), ldo >= dof.
+ * fastron_label_capsules — the geometric check that labels samples and re-labels supports
+ *   (the paper uses FCL; here capsules vs axis-aligned boxes, R12): capsules of
+ *   `radius` on the segments between consecutive entries of chain (host int32 [n_chain],
+ *   control-point indices, -1 = the base origin), boxes host double [n_cubes][6] (lo xyz,
+ *   hi xyz), n_cubes <= 64, n_chain <= 33. pos: device float4 [n_cp][ldp]. label: device
+ *   int8 [n], +1 iff any capsule touches any box (tangency counts).
+ * fastron_kernel_matvec — F = K alpha (fp64, index order over alpha != 0), the margin
+ *   vector a warm start needs when the dataset changed around a loaded alpha.
+ */
+fastron_status fastron_active_samples(const float* S, int64_t ns, int64_t lds, int32_t dof, int32_t n_near,
+                                      const float* z, const float* sigma, const float* u, int64_t n_uniform,
+                                      const float* lo, const float* hi, float* out, int64_t ldo, void* stream);
+fastron_status fastron_label_capsules(const float* pos, int64_t ldp, int64_t n, const int32_t* chain, int32_t n_chain,
+                                      const double* boxes, int32_t n_cubes, float radius, int8_t* label, void* stream);
+fastron_status fastron_kernel_matvec(const float* K, int64_t n, int64_t ldk, const double* alpha, double* F,
+                                     void* stream);
 
 /*
  * fastron_edge_check — discrete motion-planning edge check (BASELINE.json cfg4,

@@ -31,7 +31,8 @@ EXPORTED = [
     "fastron_launch_count", "fastron_model_bytes", "fastron_model_pack", "fastron_score_packed_workspace_bytes",
     "fastron_score_packed", "fastron_score_joint_workspace_bytes", "fastron_score_joint",
     "fastron_gram_joint_workspace_bytes", "fastron_gram_joint", "fastron_train_lazy_max_n",
-    "fastron_train_lazy_workspace_bytes", "fastron_train_lazy",
+    "fastron_train_lazy_workspace_bytes", "fastron_train_lazy", "fastron_active_samples", "fastron_label_capsules",
+    "fastron_kernel_matvec", "fastron_score_packed_f64",
 ]
 
 
@@ -86,6 +87,7 @@ def load_library(path: str = LIB_PATH):
     L.fastron_score_packed_workspace_bytes.argtypes = [i64, i64, i32]
     L.fastron_score_packed_workspace_bytes.restype = sz
     L.fastron_score_packed.argtypes = [vp, i64, i64, vp, i64, i32, fastron_kernel, vp, vp, vp, sz, vp]
+    L.fastron_score_packed_f64.argtypes = [vp, i64, i64, vp, i64, i32, fastron_kernel, vp, vp, sz, vp]
     L.fastron_score_joint_workspace_bytes.argtypes = [i64, i64, i32]
     L.fastron_score_joint_workspace_bytes.restype = sz
     L.fastron_score_joint.argtypes = [vp, i64, i64, vp, vp, i64, i64, i32, fastron_kernel, vp, vp, vp, sz, vp]
@@ -98,6 +100,9 @@ def load_library(path: str = LIB_PATH):
     L.fastron_train_lazy_workspace_bytes.restype = sz
     L.fastron_train_lazy.argtypes = [vp, i64, i64, i32, fastron_kernel, vp, ctypes.c_double, i64, i64, vp, vp, vp, vp,
                                      vp, i64, vp, sz, vp]
+    L.fastron_active_samples.argtypes = [vp, i64, i64, i32, i32, vp, vp, vp, i64, vp, vp, vp, i64, vp]
+    L.fastron_label_capsules.argtypes = [vp, i64, i64, vp, i32, vp, i32, ctypes.c_float, vp, vp]
+    L.fastron_kernel_matvec.argtypes = [vp, i64, i64, vp, vp, vp]
     L.fastron_gram_workspace_bytes.argtypes = [i64, i32]
     L.fastron_gram_workspace_bytes.restype = sz
     L.fastron_gram.argtypes = [vp, i64, i64, i32, fastron_kernel, vp, i64, vp, sz, vp]
@@ -111,7 +116,8 @@ def load_library(path: str = LIB_PATH):
     L.fastron_query_workspace_bytes.restype = sz
     L.fastron_query.argtypes = [rp, vp, i64, i64, vp, vp, i64, i64, fastron_kernel, vp, vp, vp, sz, vp]
     for f in ("fastron_fk", "fastron_score", "fastron_gram", "fastron_train", "fastron_edge_check", "fastron_query",
-              "fastron_model_pack", "fastron_score_packed", "fastron_score_joint", "fastron_gram_joint", "fastron_train_lazy"):
+              "fastron_model_pack", "fastron_score_packed", "fastron_score_joint", "fastron_gram_joint", "fastron_train_lazy", "fastron_active_samples",
+              "fastron_label_capsules", "fastron_kernel_matvec", "fastron_score_packed_f64"):
         getattr(L, f).restype = st
     L.fastron_last_error.argtypes = []
     L.fastron_last_error.restype = ctypes.c_char_p
@@ -254,6 +260,22 @@ def fastron_score_packed(qpos, model: PackedModel, score=None, label=None, want_
     return score, label
 
 
+def fastron_score_packed_f64(qpos, model: PackedModel, out=None, workspace=None, stream=None):
+    import torch
+    L = load_library()
+    _require_cuda(qpos)
+    M, nq = qpos.shape[0], qpos.shape[1]
+    if out is None:
+        out = torch.empty(nq, dtype=torch.float64, device=qpos.device)
+    need = L.fastron_score_packed_workspace_bytes(nq, model.ns, M)
+    if workspace is None or workspace.numel() < need:
+        workspace = _workspace(need, qpos.device)
+    _check(L.fastron_score_packed_f64(_ptr(qpos), nq, qpos.stride(0) // 4, _ptr(model.buf), model.ns, M,
+                                      _kernel(model.kind, model.gamma), _ptr(out), _ptr(workspace), workspace.numel(),
+                                      _stream(stream)))
+    return out
+
+
 def fastron_gram(pos, kind: int, gamma: float, K=None, workspace=None, stream=None):
     """pos (M, n, 4) -> K (n, n) float32 (PAPER.md:120)."""
     import torch
@@ -356,6 +378,48 @@ def fastron_train_lazy(pos, y, kind: int, gamma: float, beta: float = 1.0, iter_
                                 _ptr(tr) if tr is not None and tr is not False else None, _ptr(res), cache_cols,
                                 _ptr(workspace), workspace.numel(), _stream(stream)))
     return dict(alpha=alpha, F=F, support_idx=sup, trace=tr, result=res)
+
+
+def fastron_active_samples(S, n_near: int, z, sigma, u, lo, hi, out=None, stream=None):
+    """Two-stage active-learning draws; random numbers z ~ N(0,1), u ~ U[0,1) are inputs."""
+    import torch
+    L = load_library()
+    _require_cuda(S, z, sigma, u, lo, hi, out)
+    ns, dof = S.shape[0], S.shape[1]
+    n_uniform = u.shape[0] if u is not None else 0
+    total = ns * n_near + n_uniform
+    if out is None:
+        out = torch.empty((total, dof), dtype=torch.float32, device=S.device)
+    _check(L.fastron_active_samples(_ptr(S), ns, S.stride(0), dof, int(n_near), _ptr(z), _ptr(sigma), _ptr(u),
+                                    n_uniform, _ptr(lo), _ptr(hi), _ptr(out), out.stride(0), _stream(stream)))
+    return out
+
+
+def fastron_label_capsules(pos, chain, boxes, radius: float, label=None, stream=None):
+    """Capsule-vs-box labels (+1 = C_obs) of control-point positions pos (M, n, 4)."""
+    import torch
+    L = load_library()
+    _require_cuda(pos, label)
+    n = pos.shape[1]
+    if label is None:
+        label = torch.empty(n, dtype=torch.int8, device=pos.device)
+    ch = np.ascontiguousarray(np.asarray(chain, dtype=np.int32))
+    bx = np.ascontiguousarray(np.asarray(boxes, dtype=np.float64).reshape(-1, 6))
+    _check(L.fastron_label_capsules(_ptr(pos), pos.stride(0) // 4, n, ch.ctypes.data if len(ch) else None, len(ch),
+                                    bx.ctypes.data if len(bx) else None, len(bx), float(radius), _ptr(label),
+                                    _stream(stream)))
+    return label
+
+
+def fastron_kernel_matvec(K, alpha, F=None, stream=None):
+    import torch
+    L = load_library()
+    _require_cuda(K, alpha, F)
+    n = K.shape[0]
+    if F is None:
+        F = torch.empty(n, dtype=torch.float64, device=K.device)
+    _check(L.fastron_kernel_matvec(_ptr(K), n, K.stride(0), _ptr(alpha), _ptr(F), _stream(stream)))
+    return F
 
 
 def train_result(res_tensor) -> dict:

@@ -264,6 +264,26 @@ fastron_status fastron_score_packed(const float* qpos, int64_t nq, int64_t ldq, 
                      "fastron_score_packed");
 }
 
+fastron_status fastron_score_packed_f64(const float* qpos, int64_t nq, int64_t ldq, const void* packed, int64_t ns,
+                                        int32_t n_cp, fastron_kernel k, double* score64, void* workspace,
+                                        size_t workspace_bytes, void* stream) {
+  fastron_status s = check_kernel(k);
+  if (s != FASTRON_OK) return s;
+  FASTRON_REQUIRE(nq >= 0 && ns >= 0, "nq and ns must be >= 0");
+  FASTRON_REQUIRE(n_cp >= 1 && n_cp <= FASTRON_MAX_CP, "n_cp must be in [1,32], got %d", n_cp);
+  if (nq == 0) return FASTRON_OK;
+  FASTRON_REQUIRE(qpos && score64 && ldq >= nq, "qpos and score64 must be non-NULL and ldq >= nq");
+  FASTRON_REQUIRE(ns == 0 || packed, "packed is NULL");
+  const size_t need = fastron_score_packed_workspace_bytes(nq, ns, n_cp);
+  if (workspace_bytes < need || (need > 0 && !workspace))
+    return fail(FASTRON_ERR_WORKSPACE, "fastron_score_packed_f64 needs %zu workspace bytes, got %zu", need,
+                workspace_bytes);
+  return cuda_status(launch_score(reinterpret_cast<const float4*>(qpos), nq, ldq, static_cast<const float*>(packed), ns,
+                                  n_cp, k.kind, kernel_scale(k), nullptr, nullptr, static_cast<double*>(workspace),
+                                  S(stream), score64),
+                     "fastron_score_packed_f64");
+}
+
 size_t fastron_gram_workspace_bytes(int64_t n, int32_t n_cp) {
   if (n < 0 || n_cp < 1 || n_cp > FASTRON_MAX_CP) return 0;
   // the Gram kernel reads column tiles in pairs: round the packed buffer to an even tile count
@@ -353,6 +373,44 @@ fastron_status fastron_train_lazy(const float* pos, int64_t n, int64_t ldp, int3
     e = launch_train_lazy(packed, n, n_cp, k.kind, y, beta, iter_max, s_max, alpha_inout, F_inout, support_idx, trace,
                           result, cache, cache_cols, st);
   return cuda_status(e, "fastron_train_lazy");
+}
+
+fastron_status fastron_active_samples(const float* sup, int64_t ns, int64_t lds, int32_t dof, int32_t n_near,
+                                      const float* z, const float* sigma, const float* u, int64_t n_uniform,
+                                      const float* lo, const float* hi, float* out, int64_t ldo, void* stream) {
+  FASTRON_REQUIRE(ns >= 0 && n_near >= 0 && n_uniform >= 0, "sizes must be >= 0");
+  FASTRON_REQUIRE(dof >= 1 && dof <= FASTRON_MAX_DOF, "dof must be in [1,16], got %d", dof);
+  if (ns * n_near + n_uniform == 0) return FASTRON_OK;
+  FASTRON_REQUIRE(lo && hi && out && ldo >= dof, "lo, hi, out must be non-NULL and ldo >= dof");
+  if (ns * n_near > 0) FASTRON_REQUIRE(sup && z && sigma && lds >= dof, "S, z, sigma needed for stage-1 samples");
+  if (n_uniform > 0) FASTRON_REQUIRE(u != nullptr, "u needed for stage-2 samples");
+  return cuda_status(launch_active_samples(sup, ns, lds, dof, n_near, z, sigma, u, n_uniform, lo, hi, out, ldo, S(stream)),
+                     "fastron_active_samples");
+}
+
+fastron_status fastron_label_capsules(const float* pos, int64_t ldp, int64_t n, const int32_t* chain, int32_t n_chain,
+                                      const double* boxes, int32_t n_cubes, float radius, int8_t* label, void* stream) {
+  FASTRON_REQUIRE(n >= 0, "n must be >= 0");
+  FASTRON_REQUIRE(n_chain >= 0 && n_chain <= 33 && n_cubes >= 0 && n_cubes <= kMaxCubes,
+                  "n_chain must be in [0,33] and n_cubes in [0,64]");
+  FASTRON_REQUIRE(std::isfinite(radius) && radius >= 0.0f, "radius must be finite and >= 0");
+  if (n == 0) return FASTRON_OK;
+  FASTRON_REQUIRE(pos && label && ldp >= n, "pos and label must be non-NULL and ldp >= n");
+  FASTRON_REQUIRE(n_chain == 0 || chain, "chain is NULL");
+  FASTRON_REQUIRE(n_cubes == 0 || boxes, "boxes is NULL");
+  for (int c = 0; c < n_chain; ++c) FASTRON_REQUIRE(chain[c] >= -1 && chain[c] < FASTRON_MAX_CP, "chain[%d] invalid", c);
+  for (int b = 0; b < 6 * n_cubes; ++b) FASTRON_REQUIRE(std::isfinite(boxes[b]), "boxes contain a non-finite value");
+  return cuda_status(launch_label_capsules(reinterpret_cast<const float4*>(pos), ldp, n, chain, n_chain, boxes, n_cubes,
+                                           radius, label, S(stream)),
+                     "fastron_label_capsules");
+}
+
+fastron_status fastron_kernel_matvec(const float* K, int64_t n, int64_t ldk, const double* alpha, double* F,
+                                     void* stream) {
+  FASTRON_REQUIRE(n >= 0, "n must be >= 0");
+  if (n == 0) return FASTRON_OK;
+  FASTRON_REQUIRE(K && alpha && F && ldk >= n, "K, alpha, F must be non-NULL and ldk >= n");
+  return cuda_status(launch_matvec(K, n, ldk, alpha, F, S(stream)), "fastron_kernel_matvec");
 }
 
 size_t fastron_edge_workspace_bytes(int64_t n_edges, int64_t ns, int32_t n_cp) {

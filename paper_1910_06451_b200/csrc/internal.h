@@ -43,7 +43,8 @@ ScorePlan plan_score(int64_t nq, int64_t ns, int M, int kind);
 size_t score_partial_bytes(int64_t nq, int64_t ns, int M);
 
 cudaError_t launch_score(const float4* qpos, int64_t nq, int64_t ldq, const float* packed, int64_t ns, int M, int kind,
-                         float scale, float* score, int8_t* label, double* partial, cudaStream_t st);
+                         float scale, float* score, int8_t* label, double* partial, cudaStream_t st,
+                         double* score64 = nullptr);
 
 // K4: one round of the fused edge check (interpolate -> FK -> score -> warp vote).
 struct EdgeRound {
@@ -69,6 +70,15 @@ cudaError_t launch_joint_points(const float* x, int64_t n, int64_t ldx, int D, f
 cudaError_t launch_score_joint(const float4* qpts, int64_t nq, const float* packed, int64_t ns, int D, int kind,
                                float scale, float* score, int8_t* label, double* partial, cudaStream_t st);
 cudaError_t launch_gram_joint(const float* packed, int64_t n, int D, int kind, float* K, int64_t ldk, cudaStream_t st);
+
+// Model-update cycle pieces (update.cu)
+constexpr int kMaxCubes = 64;
+cudaError_t launch_active_samples(const float* S, int64_t ns, int64_t lds, int D, int n_near, const float* z,
+                                  const float* sigma, const float* u, int64_t n_uniform, const float* lo,
+                                  const float* hi, float* out, int64_t ldo, cudaStream_t st);
+cudaError_t launch_label_capsules(const float4* pos, int64_t ldp, int64_t n, const int32_t* chain, int n_chain,
+                                  const double* boxes, int n_cubes, float radius, int8_t* label, cudaStream_t st);
+cudaError_t launch_matvec(const float* K, int64_t n, int64_t ldk, const double* alpha, double* F, cudaStream_t st);
 
 // K3: Gram
 cudaError_t launch_gram(const float* packed, int64_t n, int M, int kind, float* K, int64_t ldk, cudaStream_t st);

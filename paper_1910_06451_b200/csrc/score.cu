@@ -114,6 +114,7 @@ struct ScoreArgs {
   uint8_t* in_collision;
   int32_t* hit_index;
   double denom;  // M for the FK kernel's 1/M mean (Eq. 4), 1 for the joint-space kernel
+  double* score64;  // optional fp64 scores (margins for a warm start)
 };
 
 // Position k of the visiting order of round r, lane l: evens first, then odds (R11).
@@ -338,6 +339,7 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
     } else if (MODE == MODE_POS || MODE == MODE_JOINT) {
       if (vq < A.nq) {
         const double fm = f[j] / A.denom;
+        if (A.score64) A.score64[vq] = fm;
         if (A.score) A.score[vq] = (float)fm;
         if (A.label) A.label[vq] = fm > 0.0 ? 1 : -1;
       }
@@ -362,6 +364,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ S
     for (int s = 0; s < A.n_splits; ++s) f += A.partial[(int64_t)s * A.nq + vq];
   const double fm = f / A.denom;
   if (MODE == MODE_POS || MODE == MODE_JOINT) {
+    if (A.score64) A.score64[vq] = fm;
     if (A.score) A.score[vq] = (float)fm;
     if (A.label) A.label[vq] = fm > 0.0 ? 1 : -1;
   } else {
@@ -534,9 +537,11 @@ ScorePlan plan_score(int64_t nq, int64_t ns, int M, int kind) {
 }
 
 cudaError_t launch_score(const float4* qpos, int64_t nq, int64_t ldq, const float* packed, int64_t ns, int M, int kind,
-                         float scale, float* score, int8_t* label, double* partial, cudaStream_t st) {
+                         float scale, float* score, int8_t* label, double* partial, cudaStream_t st,
+                         double* score64) {
   if (nq <= 0) return cudaSuccess;
   ScoreArgs A = {};
+  A.score64 = score64;
   A.qpos = qpos;
   A.ldq = ldq;
   A.nq = nq;

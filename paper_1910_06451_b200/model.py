@@ -1,0 +1,95 @@
+"""FastronModel — host orchestration of the C-ABI calls into the paper's workflow:
+fit (Algorithm 1 on a labelled dataset), query (the proxy collision check) and update
+(the two-stage active-learning cycle of PAPER.md:272 followed by a warm-started
+Algorithm 1). Every arithmetic step runs in the library's kernels; this
+module only allocates device tensors and sequences the calls.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Optional
+
+import numpy as np
+
+from . import (fastron_active_samples, fastron_fk, fastron_gram, fastron_kernel_matvec, fastron_label_capsules,
+               fastron_model_pack, fastron_score_packed, fastron_score_packed_f64, fastron_train, fastron_train_lazy,
+               make_robot_struct, train_result)
+
+
+@dataclasses.dataclass
+class CapsuleScene:
+    """Geometric checker of the update cycle (the paper's FCL; here capsules vs boxes, R12)."""
+
+    chain: np.ndarray  # int32 control-point indices (-1 = base origin)
+    boxes: np.ndarray  # (n, 2, 3) or (n, 6) float64 lo/hi corners
+    radius: float
+
+    def flat_boxes(self) -> np.ndarray:
+        return np.asarray(self.boxes, dtype=np.float64).reshape(-1, 6)
+
+
+class FastronModel:
+    def __init__(self, robot, kind: int = 0, gamma: float = 5.0, beta: float = 1.0, iter_max: int = 20000,
+                 s_max: Optional[int] = None, lazy: bool = False, cache_cols: int = 4096):
+        self.robot = robot
+        self.robot_c = make_robot_struct(robot)
+        self.kind, self.gamma, self.beta = int(kind), float(gamma), float(beta)
+        self.iter_max, self.s_max, self.lazy, self.cache_cols = int(iter_max), s_max, bool(lazy), int(cache_cols)
+        self.supports = None  # (|S|, D) device float32 configurations
+        self.alpha = None  # (|S|,) device float64
+        self.last = None  # result dict of the last training run
+
+    # ---- Algorithm 1 on a dataset ----
+    def _train(self, X, y, alpha0=None, F0=None):
+        import torch
+        pos = fastron_fk(self.robot_c, X)
+        n = X.shape[0]
+        s_max = n if self.s_max is None else self.s_max
+        if self.lazy:
+            if alpha0 is not None and F0 is None:  # margins of the loaded model: F = K alpha = f(X)
+                F0 = fastron_score_packed_f64(pos, self.model)
+            out = fastron_train_lazy(pos, y, self.kind, self.gamma, self.beta, self.iter_max, s_max, alpha=alpha0, F=F0,
+                                     cache_cols=min(self.cache_cols, n))
+        else:
+            K = fastron_gram(pos, self.kind, self.gamma)
+            if alpha0 is not None and F0 is None:
+                F0 = fastron_kernel_matvec(K, alpha0)
+            out = fastron_train(K, y, self.beta, self.iter_max, s_max, alpha=alpha0, F=F0)
+        res = train_result(out["result"])
+        sup = out["support_idx"][:res["n_support"]].long()
+        self.supports = X[sup].contiguous()
+        self.alpha = out["alpha"][sup].contiguous()
+        self.labels = y[sup].contiguous()
+        self.last = dict(res, n=n)
+        self._pack()
+        return self.last
+
+    def _pack(self):
+        spos = fastron_fk(self.robot_c, self.supports)
+        self.model = fastron_model_pack(spos, self.alpha.float(), self.kind, self.gamma)
+
+    def fit(self, X, y):
+        """X: (N, D) float32 device configurations, y: (N,) int8 device labels (+1 = C_obs)."""
+        return self._train(X, y)
+
+    # ---- proxy collision check ----
+    def query(self, q):
+        qpos = fastron_fk(self.robot_c, q)
+        return fastron_score_packed(qpos, self.model)
+
+    # ---- the update cycle ----
+    def update(self, scene: CapsuleScene, z, u, sigma, lo, hi, n_near: int):
+        """Stage 1: n_near draws around every support point (z ~ N(0,1) inputs, scale sigma);
+        stage 2: uniform draws (u ~ U[0,1) inputs). The support points and the new samples
+        are labelled by the geometric check, then Algorithm 1 restarts from the previous
+        alpha (loadPreviousModel) on that dataset."""
+        import torch
+        samples = fastron_active_samples(self.supports, n_near, z, sigma, u, lo, hi)
+        X = torch.cat([self.supports, samples], dim=0).contiguous()
+        pos = fastron_fk(self.robot_c, X)
+        y = fastron_label_capsules(pos, scene.chain, scene.flat_boxes(), scene.radius)
+        # loadPreviousModel: the support points keep their alpha, new samples start at 0
+        alpha0 = torch.zeros(X.shape[0], dtype=torch.float64, device=X.device)
+        alpha0[:self.supports.shape[0]] = self.alpha
+        a_in = alpha0.clone()
+        return self._train(X, y, alpha0=alpha0), X, y, a_in
