@@ -28,6 +28,7 @@
 // (R13). removeNonsupportPoints is an ordered compaction.
 #include <cooperative_groups.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "fastron_device.cuh"
@@ -112,14 +113,21 @@ __device__ __forceinline__ int warp_argbest(uint64_t key, int idx, uint64_t& bke
   const unsigned full = 0xffffffffu;
   const bool live = idx != kNone;
   const uint32_t h = (uint32_t)(key >> 32), l = (uint32_t)key;
-  uint32_t bh, bl;
-  if (MAX_KEY) {
-    bh = __reduce_max_sync(full, live ? h : 0u);
-    bl = __reduce_max_sync(full, (live && h == bh) ? l : 0u);
-  } else {
-    bh = __reduce_min_sync(full, live ? h : 0xffffffffu);
-    bl = __reduce_min_sync(full, (live && h == bh) ? l : 0xffffffffu);
+  const uint32_t bh = MAX_KEY ? __reduce_max_sync(full, live ? h : 0u) : __reduce_min_sync(full, live ? h : 0xffffffffu);
+  const unsigned hmask = __ballot_sync(full, live && h == bh);
+  if (__popc(hmask) == 1) {  // common case: the high word alone decides (one REDUX + one vote)
+    const int wl = __ffs(hmask) - 1;
+    bidx = __shfl_sync(full, idx, wl);
+    bkey = ((uint64_t)bh << 32) | __shfl_sync(full, l, wl);
+    return wl;
   }
+  if (hmask == 0u) {  // every lane empty
+    bidx = kNone;
+    bkey = MAX_KEY ? 0ull : ~0ull;
+    return -1;
+  }
+  const uint32_t bl = MAX_KEY ? __reduce_max_sync(full, (live && h == bh) ? l : 0u)
+                              : __reduce_min_sync(full, (live && h == bh) ? l : 0xffffffffu);
   const bool eq = live && h == bh && l == bl;
   bidx = (int)__reduce_min_sync(full, eq ? (unsigned)idx : (unsigned)kNone);
   bkey = ((uint64_t)bh << 32) | bl;
@@ -217,7 +225,6 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
   __shared__ Cand s_warp[2][kTrainWarps];
   __shared__ Cand s_cta[2];
   __shared__ int32_t s_cta_cnt[2];
-  __shared__ Decision s_dec[2];
   __shared__ int32_t s_cnt[kTrainWarps];
 
   const int lo = rank * (int)A.chunk;
@@ -284,6 +291,20 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
   int parity = 0;
   int converged = 0;
 
+#ifdef FASTRON_TRAIN_PROF
+  unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long tp = clock64();
+#define PROF_MARK(i)                         \
+  do {                                       \
+    const unsigned long long tn = clock64(); \
+    prof[i] += tn - tp;                      \
+    tp = tn;                                 \
+  } while (0)
+#else
+#define PROF_MARK(i) \
+  do {               \
+  } while (0)
+#endif
   for (;;) {
     // ---- 1. all loads of the pending K row, then the fused update + min scan ----
     float kr[EPT];
@@ -340,6 +361,7 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
         if (G[k] < m0) { m0 = G[k]; k0 = k; }
       }
     }
+    PROF_MARK(0);
     // merge (slot order == index order inside a thread; the lower slot wins ties)
     double mk = m0;
     int mkk = k0;
@@ -348,7 +370,10 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
     {
       uint64_t wkey;
       int widx;
-      const int wl = warp_argbest<false>(order_key(mk), my_idx, wkey, widx);
+      const uint64_t okey = order_key(mk);
+      PROF_MARK(6);
+      const int wl = warp_argbest<false>(okey, my_idx, wkey, widx);
+      PROF_MARK(7);
       if (lane == wl) {  // the owner lane attaches the payload of the warp winner
         const int jw = mkk * kTrainNT + tid;
         s_warp[parity][warp] = Cand{wkey, mk, s_Y[jw], widx, ((yneg >> mkk) & 1u) ? -1 : 1, LAZY ? s_slot[jw] : -1, 0};
@@ -356,26 +381,28 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
         s_warp[parity][warp] = cand_none(false);
       }
     }
+    PROF_MARK(1);
     __syncthreads();
+    PROF_MARK(2);
 
-    // ---- 2. warp 0: CTA (and cluster) reduction + the decision of Algorithm 1 ----
-    if (warp == 0) {
+    // ---- 2. CTA (and cluster) reduction + the decision of Algorithm 1, taken redundantly
+    //         by every warp (identical inputs -> identical decisions, no second barrier;
+    //         the candidate buffers are double-buffered by parity) ----
+    Decision d;
+    if (C == 1) {
       const Cand best = warp_best<false>(lane < kTrainWarps ? s_warp[parity][lane] : cand_none(false));
-      if (C == 1) {
-        if (lane == 0) s_dec[parity] = decide_min(best, iters, nnz, nfree, A);
-      } else if (lane == 0) {
-        s_cta[parity] = best;
-      }
-    }
-    if (C > 1) {
-      cluster.sync();
+      d = decide_min(best, iters, nnz, nfree, A);
+    } else {
       if (warp == 0) {
-        const Cand best = warp_best<false>(lane < C ? *cluster.map_shared_rank(&s_cta[parity], lane) : cand_none(false));
-        if (lane == 0) s_dec[parity] = decide_min(best, iters, nnz, nfree, A);
+        const Cand best = warp_best<false>(lane < kTrainWarps ? s_warp[parity][lane] : cand_none(false));
+        if (lane == 0) s_cta[parity] = best;
       }
+      cluster.sync();
+      const Cand best = warp_best<false>(lane < C ? *cluster.map_shared_rank(&s_cta[parity], lane) : cand_none(false));
+      d = decide_min(best, iters, nnz, nfree, A);
     }
-    __syncthreads();
-    Decision d = s_dec[parity];
+    PROF_MARK(3);
+    PROF_MARK(4);
 
     // ---- 3. only when the add branch does not `continue`: the removal scan ----
     if (d.action == ACT_CHECK_REMOVAL) {
@@ -404,23 +431,18 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
         }
       }
       __syncthreads();
-      if (warp == 0) {
+      if (C == 1) {
         const Cand best = warp_best<true>(lane < kTrainWarps ? s_warp[q][lane] : cand_none(true));
-        if (C == 1) {
-          if (lane == 0) s_dec[q] = decide_removal(d, best, nfree, A);
-        } else if (lane == 0) {
-          s_cta[q] = best;
-        }
-      }
-      if (C > 1) {
-        cluster.sync();
+        d = decide_removal(d, best, nfree, A);
+      } else {
         if (warp == 0) {
-          const Cand best = warp_best<true>(lane < C ? *cluster.map_shared_rank(&s_cta[q], lane) : cand_none(true));
-          if (lane == 0) s_dec[q] = decide_removal(d, best, nfree, A);
+          const Cand best = warp_best<true>(lane < kTrainWarps ? s_warp[q][lane] : cand_none(true));
+          if (lane == 0) s_cta[q] = best;
         }
+        cluster.sync();
+        const Cand best = warp_best<true>(lane < C ? *cluster.map_shared_rank(&s_cta[q], lane) : cand_none(true));
+        d = decide_removal(d, best, nfree, A);
       }
-      __syncthreads();
-      d = s_dec[q];
       parity = q;  // buffers of parity q were used last; the loop flips back below
     }
 
@@ -428,6 +450,7 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
       converged = d.converged;
       break;
     }
+    PROF_MARK(5);
     // apply the step: the owner thread updates Y_i, everyone records the pending
     // rank-one update of G for the next pass
     if (d.idx >= lo && d.idx < hi && ((d.idx - lo) % kTrainNT) == tid) {
@@ -449,6 +472,13 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
     parity ^= 1;
   }
 
+#ifdef FASTRON_TRAIN_PROF
+  if (tid == 0 && rank == 0)
+    printf("train prof cycles/iter: scan %.0f merge+key %.0f argbest %.0f payload %.0f bar %.0f decide %.0f - %.0f tail %.0f (iters %lld)\n",
+           (double)prof[0] / iters, (double)prof[6] / iters, (double)prof[7] / iters, (double)prof[1] / iters,
+           (double)prof[2] / iters, (double)prof[3] / iters, (double)prof[4] / iters, (double)prof[5] / iters,
+           (long long)iters);
+#endif
   // ---- write back (F = y G, alpha = y Y) + removeNonsupportPoints ----
   int cnt = 0;
 #pragma unroll

@@ -1,1 +1,3 @@
-timeout 900 python bench.py --steps 5 --warmup 3 --rows --no-cpu > gpurun_out/bench_rows.log 2>&1; tail -3 gpurun_out/bench_rows.log | python -c "import json,sys; l=sys.stdin.read().strip().splitlines(); d=json.loads(l[-1]); print(json.dumps(d['rows']['cfg3_update_cycle'])); print(d['value'])" || tail -20 gpurun_out/bench_rows.log
+for n in 512 5000; do TRAIN_N=$n FASTRON_LIB=build/variants/lib_trprof.so timeout 300 python tools/train_sweep.py 1 2>&1 | grep -E "prof" | head -1; done
+timeout 900 python -m pytest tests/test_gpu_gram_train.py tests/test_gpu_lazy.py tests/test_gpu_update.py -q --timeout=300 -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; tail -1 gpurun_out/gpu_tests.log
+TRAIN_N=5000 timeout 300 python tools/train_sweep.py 1 2 4 2>&1 | tail -3
