@@ -2,16 +2,17 @@
 // Algorithm 1's "computeKernelMatrixColumn").
 //
 // Upper-triangular 128x128 tiles (bi <= bj), one CTA of 4 warps per tile:
-//  * COLUMN points live in registers: each lane holds CPL columns (4 at M <= 8, 2 at
-//    M <= 16) as pre-scaled f32x2 control-point pairs (the packed records of the
-//    scoring kernel); a warp covers 32*CPL columns;
+//  * COLUMN points live in registers: each lane holds CPL consecutive columns (4 at
+//    M <= 8, 2 at M <= 16) as pre-scaled f32x2 control-point pairs (the packed records of
+//    the scoring kernel); a warp covers 32*CPL columns;
 //  * the tile's 128 ROW points arrive as two packed support tiles by one TMA bulk copy;
 //    each warp walks a contiguous row range; a row record is a warp-broadcast
 //    LDS.128 + LDS.64 shared by the lane's CPL columns;
-//  * the (bi, bj) block is stored straight from registers: for a fixed row the 32 lanes
-//    write 32 consecutive floats (coalesced). The mirrored (bj, bi) block goes through a
-//    per-warp (32*CPL)x9 shared-memory transpose buffer, 8 rows at a time, and is written
-//    as one 32-byte segment (two float4) per column.
+//  * the (bi, bj) block is stored straight from registers: for a fixed row each lane
+//    writes its CPL consecutive floats as one vector store (the warp covers 32*CPL
+//    consecutive floats). The lane keeps its last 8 rows x CPL values in registers and
+//    writes the mirrored (bj, bi) block from them: one 32-byte segment (two float4) per
+//    column per 8 rows — no shared-memory transpose, one store per row per lane.
 // JOINT = true builds the joint-space RBF Gram of the "Fastron RBF" baseline (PAPER.md:37,
 // :114-117) from zero-padded pseudo points: one RBF term of the whole squared distance.
 // The same term_pair() and control-point summation order as fastron_score make K_ij
@@ -32,8 +33,10 @@ namespace fastron {
 constexpr int kGT = 32 * FASTRON_GRAM_WARPS;  // threads per Gram CTA
 constexpr int kGW = kGT / 32;
 constexpr int kGB = 128;             // tile edge (2 support tiles)
-constexpr int kChunkRows = 8;        // rows per mirror-transpose chunk
-constexpr int kMS = kChunkRows + 1;  // padded stride of the transpose buffer
+#ifndef FASTRON_GRAM_CHUNK
+#define FASTRON_GRAM_CHUNK 4
+#endif
+constexpr int kChunkRows = FASTRON_GRAM_CHUNK;  // rows per mirror chunk (held in registers): 4 or 8
 
 __device__ __forceinline__ void tile_coords(int64_t t, int64_t nb, int64_t& bi, int64_t& bj) {
   // row-major enumeration of the upper triangle: row bi holds tiles bi..nb-1
@@ -64,7 +67,6 @@ __global__ void __launch_bounds__(kGT) gram_kernel(const float* __restrict__ pac
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
   float* rows = reinterpret_cast<float*>(smem_raw + 128);  // 2 packed tiles
-  float* tbuf = rows + 2 * TF;                               // [kGW][WC][kMS]
 
   const int64_t nb = (n + kGB - 1) / kGB;
   int64_t bi, bj;
@@ -87,11 +89,11 @@ __global__ void __launch_bounds__(kGT) gram_kernel(const float* __restrict__ pac
     for (int c = 0; c < rt; ++c) tma_bulk_g2s(rows + c * TF, packed + (2 * bi + c) * TF, TB, bar);
   }
 
-  // the lane's CPL columns, read from the same packed (scaled) records
+  // the lane's CPL consecutive columns cbase + CPL*lane + h, read from the packed (scaled) records
   f2 ux[CPL][NP], uy[CPL][NP], uz[CPL][NP];
 #pragma unroll
   for (int h = 0; h < CPL; ++h) {
-    const int64_t j = j0 + cbase + lane + 32 * h;
+    const int64_t j = j0 + cbase + CPL * lane + h;
     const int64_t jj = j < n ? j : 0;
     const float* rec = packed + (jj / kTileSupports) * TF + (jj % kTileSupports) * NP * 8;
 #pragma unroll
@@ -106,13 +108,17 @@ __global__ void __launch_bounds__(kGT) gram_kernel(const float* __restrict__ pac
   mbar_wait(bar, 0);
 
   const bool mirror = bi != bj;
-  float* tb = tbuf + warp * (WC * kMS);
   const int rows_here = (int)min((int64_t)kGB, n - i0);
+  const int64_t c0 = j0 + cbase + CPL * lane;  // the lane's first column
+  const bool cols_full = c0 + CPL <= n;
+  // vector stores need CPL-float (direct) and 32-byte (mirror) alignment of the rows
+  const bool vec_ok = (ldk % 8) == 0 && (reinterpret_cast<uintptr_t>(K) & 31) == 0;
   // fixed trip counts (no early exits) so loads of the next row overlap this row's math;
   // rows past the matrix edge are computed on stale shared memory but never stored
   const int q_end = min(RW, ((rows_here - rbase + kChunkRows - 1) / kChunkRows) * kChunkRows);
   for (int q0 = 0; q0 < q_end; q0 += kChunkRows) {
-#pragma unroll 2
+    float v[kChunkRows][CPL];  // 8 rows x CPL columns: the chunk, kept for the mirror block
+#pragma unroll
     for (int qq = 0; qq < kChunkRows; ++qq) {
       const int r = rbase + q0 + qq;
       const float* rec = rows + (r / kTileSupports) * TF + (r % kTileSupports) * NP * 8;
@@ -141,52 +147,64 @@ __global__ void __launch_bounds__(kGT) gram_kernel(const float* __restrict__ pac
           }
         }
       }
-      float* Krow = K + (i0 + r) * ldk + j0 + cbase;
 #pragma unroll
       for (int h = 0; h < CPL; ++h) {
-        float v;
+        float x;
         if (JOINT) {
           const float d2 = pair_sum(acc[h]);
           if (KIND == kGaussian) {
-            v = ex2_neg(d2);
+            x = ex2_neg(d2);
           } else {
             const float w = 1.0f + d2;
-            v = rcp_approx(w * w);
+            x = rcp_approx(w * w);
           }
         } else {
           const float ks = pair_sum(acc[h]);
-          v = m_pow2 ? ks * inv_m : __fdiv_rn(ks, (float)M);
+          x = m_pow2 ? ks * inv_m : __fdiv_rn(ks, (float)M);
         }
-        const int c = lane + 32 * h;
-        if (r < rows_here && j0 + cbase + c < n) Krow[c] = v;  // direct block, coalesced across the warp
-        tb[c * kMS + qq] = v;                  // transposed copy for the mirror block
+        v[qq][h] = x;
+      }
+      // direct block: row i0 + r, the lane's CPL consecutive columns (the warp writes
+      // 32*CPL consecutive floats)
+      if (r < rows_here) {
+        float* Kd = K + (i0 + r) * ldk + c0;
+        if (CPL == 4 && vec_ok && cols_full) {
+          *reinterpret_cast<float4*>(Kd) = make_float4(v[qq][0], v[qq][CPL > 1 ? 1 : 0], v[qq][CPL > 2 ? 2 : 0],
+                                                       v[qq][CPL > 3 ? 3 : 0]);
+        } else if (CPL == 2 && vec_ok && cols_full) {
+          *reinterpret_cast<float2*>(Kd) = make_float2(v[qq][0], v[qq][CPL > 1 ? 1 : 0]);
+        } else {
+#pragma unroll
+          for (int h = 0; h < CPL; ++h)
+            if (c0 + h < n) Kd[h] = v[qq][h];
+        }
       }
     }
     if (mirror) {
-      __syncwarp();
-      // mirror block: row j0 + cbase + c, columns i0 + rbase + q0 .. +7 (one 32-byte segment)
+      // mirror block: row c0 + h, columns i0 + rbase + q0 .. +7 (one 32-byte segment)
       const int nrow = min(kChunkRows, rows_here - (rbase + q0));
 #pragma unroll
       for (int h = 0; h < CPL; ++h) {
-        const int c = lane + 32 * h;
-        if (j0 + cbase + c >= n) continue;
-        float* Kr = K + (j0 + cbase + c) * ldk + i0 + rbase + q0;
-        const float* src = tb + c * kMS;
-        if (nrow == kChunkRows && ((reinterpret_cast<uintptr_t>(Kr) & 15) == 0)) {
-          reinterpret_cast<float4*>(Kr)[0] = make_float4(src[0], src[1], src[2], src[3]);
-          reinterpret_cast<float4*>(Kr)[1] = make_float4(src[4], src[5], src[6], src[7]);
+        if (c0 + h >= n) continue;
+        float* Kr = K + (c0 + h) * ldk + i0 + rbase + q0;
+        if (nrow == kChunkRows && vec_ok) {
+#pragma unroll
+          for (int k4 = 0; k4 < kChunkRows / 4; ++k4)
+            reinterpret_cast<float4*>(Kr)[k4] =
+                make_float4(v[4 * k4][h], v[4 * k4 + 1][h], v[4 * k4 + 2][h], v[4 * k4 + 3][h]);
         } else {
-          for (int qq = 0; qq < nrow; ++qq) Kr[qq] = src[qq];
+#pragma unroll
+          for (int qq = 0; qq < kChunkRows; ++qq)
+            if (qq < nrow) Kr[qq] = v[qq][h];
         }
       }
-      __syncwarp();
     }
   }
 }
 
 template <int MP, int KIND, bool JOINT = false>
 static cudaError_t run_gram(const float* packed, int64_t n, int M, float* K, int64_t ldk, cudaStream_t st) {
-  const size_t smem = 128 + 2 * tile_bytes(MP) + (size_t)kGW * 32 * gram_cpl(MP) * kMS * 4;
+  const size_t smem = 128 + 2 * tile_bytes(MP);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gram_kernel<MP, KIND, JOINT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
