@@ -141,3 +141,29 @@ def test_train_hand_derived_cases(case):
     _assert_same_run(g, r)
     np.testing.assert_allclose(g["alpha"], case["alpha"], atol=1e-6)
     assert g["trace"].tolist() == case["trace"]
+
+
+def test_cfg5_gram_full_size_sampled_rows():
+    """cfg5 Gram at full size (N = 20,000, M = 16, 1.6 GB): 200 seeded rows against the
+    oracle's Eq. 4 values (each row = the oracle score of all N points against one support
+    with alpha = 1, i.e. K(x_j, x_i) by its definition), plus exact symmetry of those rows
+    and columns and the unit diagonal."""
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    robot, X = W.cfg5_gram_workload()[:2]
+    assert X.shape == (20_000, 7) and robot.n_cp == 16
+    pos = fb.fastron_fk(robot, dev(X))
+    K = fb.fastron_gram(pos, 0, 5.0)
+    torch.cuda.synchronize()
+    rows = np.random.default_rng(11).choice(len(X), 200, replace=False)
+    rows[-1] = len(X) - 1  # the ragged last tile
+    Kr = K[torch.as_tensor(rows, device=K.device)].cpu().numpy()
+    Kc = K[:, torch.as_tensor(rows, device=K.device)].cpu().numpy().T
+    del K
+    assert np.array_equal(Kr, Kc)
+    assert np.all(Kr[np.arange(len(rows)), rows] == 1.0)
+    opos = oracle.fk(robot, X)
+    for r, i in enumerate(rows):
+        ref, _ = oracle.score(0, 5.0, opos, opos[i:i + 1], np.ones(1, np.float32))
+        assert_score_parity(Kr[r], ref, what=f"cfg5 Gram row {i}")

@@ -164,3 +164,16 @@ def test_query_host_pipeline_matches_device_path():
     fb.fastron_query(wl.robot, dev(wl.queries[:1000]), spos, alpha, 0, wl.gamma, score=sd)
     torch.cuda.synchronize()
     assert np.array_equal(sd.cpu().numpy(), s_dev[:1000])
+
+
+def test_cfg5_full_size_sampled():
+    """cfg5 at its full BASELINE.json size (10M queries x 20k supports, M = 16): the oracle
+    recomputes a seeded sample of 1,000 queries plus the 500 GPU scores nearest zero."""
+    require_gpu()
+    wl = W.score_workload("cfg5")
+    assert len(wl.queries) == 10_000_000 and len(wl.supports) == 20_000 and wl.robot.n_cp == 16
+    s, l = _gpu_scores(wl.robot, wl.supports, wl.alpha, wl.queries, 0, wl.gamma)
+    rng = np.random.default_rng(5)
+    idx = np.unique(np.concatenate([rng.choice(len(s), 1000, replace=False), np.argsort(np.abs(s))[:500]]))
+    f, _ = _ref_scores(wl.robot, wl.supports, wl.alpha, wl.queries[idx], 0, wl.gamma)
+    assert_score_parity(s[idx], f, l[idx], what="cfg5 full-size sample")
