@@ -23,7 +23,11 @@
  *    CUDA launch/runtime failure returns FASTRON_ERR_CUDA. fastron_last_error()
  *    returns a thread-local message for the last non-OK status of the calling thread.
  *  - Device array CONTENTS (NaN joint values, labels outside {-1,+1}) are not
- *    checked on the hot path.
+ *    checked on the hot path. With validation on (fastron_set_validation(1), or the
+ *    environment variable FASTRON_VALIDATE=1 at the first call) every entry point
+ *    first counts non-finite values in its float inputs and labels outside {-1,+1},
+ *    synchronising `stream` to read the count, and returns FASTRON_ERR_INVALID_ARG if
+ *    any is found (SURVEY §8(b) conventions). A debugging aid, off by default.
  *  - There is no CPU fallback: every computation runs in this library's kernels.
  *
  * Data layouts
@@ -287,6 +291,11 @@ const char* fastron_last_error(void);
  * (a counter for the bench's gpu_launches claim). */
 const char* fastron_version(void);
 int64_t fastron_launch_count(void);
+
+/* Content validation switch (see Conventions): on != 0 enables it for the process,
+ * 0 disables it; fastron_validation() returns the current setting. */
+void fastron_set_validation(int32_t on);
+int32_t fastron_validation(void);
 
 #ifdef __cplusplus
 }

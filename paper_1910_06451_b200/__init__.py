@@ -32,7 +32,7 @@ EXPORTED = [
     "fastron_score_packed", "fastron_score_joint_workspace_bytes", "fastron_score_joint",
     "fastron_gram_joint_workspace_bytes", "fastron_gram_joint", "fastron_train_lazy_max_n",
     "fastron_train_lazy_workspace_bytes", "fastron_train_lazy", "fastron_active_samples", "fastron_label_capsules",
-    "fastron_kernel_matvec", "fastron_score_packed_f64",
+    "fastron_kernel_matvec", "fastron_score_packed_f64", "fastron_set_validation", "fastron_validation",
 ]
 
 
@@ -125,6 +125,10 @@ def load_library(path: str = LIB_PATH):
     L.fastron_version.restype = ctypes.c_char_p
     L.fastron_launch_count.argtypes = []
     L.fastron_launch_count.restype = i64
+    L.fastron_set_validation.argtypes = [i32]
+    L.fastron_set_validation.restype = None
+    L.fastron_validation.argtypes = []
+    L.fastron_validation.restype = i32
     _lib = L
     return L
 
@@ -475,6 +479,15 @@ def fastron_query(robot, q, spos, alpha, kind: int, gamma: float, score=None, la
 
 def launch_count() -> int:
     return int(load_library().fastron_launch_count())
+
+
+def set_validation(on: bool) -> None:
+    """Content validation of every entry point's inputs (include/fastron.h conventions)."""
+    load_library().fastron_set_validation(1 if on else 0)
+
+
+def validation() -> bool:
+    return bool(load_library().fastron_validation())
 
 
 def version() -> str:

@@ -71,6 +71,54 @@ fastron_status cuda_status(cudaError_t e, const char* where) {
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// ---- optional content validation (fastron_set_validation, FASTRON_VALIDATE=1) ----
+std::atomic<int> g_validate{-1};
+
+bool validation_on() {
+  int v = g_validate.load();
+  if (v < 0) {
+    const char* e = getenv("FASTRON_VALIDATE");
+    v = (e && e[0] == '1') ? 1 : 0;
+    g_validate.store(v);
+  }
+  return v == 1;
+}
+
+fastron_status vcheck_f32(const float* a, int64_t rows, int64_t cols, int64_t ld, void* stream, const char* what) {
+  if (!a) return FASTRON_OK;
+  unsigned long long bad = 0;
+  const cudaError_t e = count_nonfinite(a, rows, cols, ld, S(stream), &bad);
+  if (e != cudaSuccess) return fail(FASTRON_ERR_CUDA, "validation of %s: %s", what, cudaGetErrorString(e));
+  if (bad) return fail(FASTRON_ERR_INVALID_ARG, "validation: %s holds %llu non-finite values", what, bad);
+  return FASTRON_OK;
+}
+
+fastron_status vcheck_f64(const double* a, int64_t n, void* stream, const char* what) {
+  if (!a) return FASTRON_OK;
+  unsigned long long bad = 0;
+  const cudaError_t e = count_nonfinite_f64(a, n, S(stream), &bad);
+  if (e != cudaSuccess) return fail(FASTRON_ERR_CUDA, "validation of %s: %s", what, cudaGetErrorString(e));
+  if (bad) return fail(FASTRON_ERR_INVALID_ARG, "validation: %s holds %llu non-finite values", what, bad);
+  return FASTRON_OK;
+}
+
+fastron_status vcheck_labels(const int8_t* y, int64_t n, void* stream) {
+  if (!y) return FASTRON_OK;
+  unsigned long long bad = 0;
+  const cudaError_t e = count_bad_labels(y, n, S(stream), &bad);
+  if (e != cudaSuccess) return fail(FASTRON_ERR_CUDA, "validation of y: %s", cudaGetErrorString(e));
+  if (bad) return fail(FASTRON_ERR_INVALID_ARG, "validation: y holds %llu labels outside {-1, +1}", bad);
+  return FASTRON_OK;
+}
+
+#define FASTRON_VALIDATE(expr)                  \
+  do {                                          \
+    if (validation_on()) {                      \
+      const fastron_status vs_ = (expr);        \
+      if (vs_ != FASTRON_OK) return vs_;        \
+    }                                           \
+  } while (0)
+
 fastron_status check_kernel(const fastron_kernel& k) {
   FASTRON_REQUIRE(k.kind == FASTRON_RBF_GAUSSIAN || k.kind == FASTRON_RBF_RQ, "kernel kind %d is not a fastron_rbf", k.kind);
   FASTRON_REQUIRE(std::isfinite(k.gamma) && k.gamma > 0.0f, "gamma must be finite and > 0 (PAPER.md:118), got %g",
@@ -165,6 +213,10 @@ const char* fastron_version(void) { return "fastron_b200 0.1.0 (sm_100a)"; }
 
 int64_t fastron_launch_count(void) { return g_launches.load(); }
 
+void fastron_set_validation(int32_t on) { g_validate.store(on ? 1 : 0); }
+
+int32_t fastron_validation(void) { return validation_on() ? 1 : 0; }
+
 fastron_status fastron_fk(const fastron_robot* robot, const float* q, int64_t n, int64_t ldq, float* pos, int64_t ldpos,
                           void* stream) {
   fastron_status s = check_robot(robot);
@@ -175,6 +227,7 @@ fastron_status fastron_fk(const fastron_robot* robot, const float* q, int64_t n,
   FASTRON_REQUIRE(ldq >= robot->dof, "ldq (%lld) < dof (%d)", (long long)ldq, robot->dof);
   FASTRON_REQUIRE(ldpos >= n, "ldpos (%lld) < n (%lld)", (long long)ldpos, (long long)n);
   FASTRON_REQUIRE(((uintptr_t)pos & 15) == 0, "pos must be 16-byte aligned");
+  FASTRON_VALIDATE(vcheck_f32(q, n, robot->dof, ldq, stream, "q"));
   return cuda_status(launch_fk(make_fk_params(*robot), q, n, ldq, reinterpret_cast<float4*>(pos), ldpos, S(stream)),
                      "fastron_fk");
 }
@@ -203,6 +256,11 @@ fastron_status fastron_score(const float* qpos, int64_t nq, int64_t ldq, const f
   if (workspace_bytes < need || (need > 0 && !workspace))
     return fail(FASTRON_ERR_WORKSPACE, "fastron_score needs %zu workspace bytes, got %zu", need, workspace_bytes);
   FASTRON_REQUIRE(((uintptr_t)workspace & 255) == 0, "workspace must be 256-byte aligned");
+  FASTRON_VALIDATE(vcheck_f32(qpos, n_cp, 4 * nq, 4 * ldq, stream, "qpos"));
+  if (ns > 0) {
+    FASTRON_VALIDATE(vcheck_f32(spos, n_cp, 4 * ns, 4 * lds, stream, "spos"));
+    FASTRON_VALIDATE(vcheck_f32(alpha, 1, ns, ns, stream, "alpha"));
+  }
   char* ws = static_cast<char*>(workspace);
   float* packed = reinterpret_cast<float*>(ws);
   double* partial = reinterpret_cast<double*>(ws + align_up(packed_bytes(ns, n_cp)));
@@ -232,6 +290,8 @@ fastron_status fastron_model_pack(const float* spos, const float* alpha, int64_t
   if (packed_bytes_given < need || !packed)
     return fail(FASTRON_ERR_WORKSPACE, "fastron_model_pack needs %zu bytes, got %zu", need, packed_bytes_given);
   FASTRON_REQUIRE(((uintptr_t)packed & 255) == 0, "packed must be 256-byte aligned");
+  FASTRON_VALIDATE(vcheck_f32(spos, n_cp, 4 * ns, 4 * lds, stream, "spos"));
+  FASTRON_VALIDATE(vcheck_f32(alpha, 1, ns, ns, stream, "alpha"));
   return cuda_status(launch_pack(reinterpret_cast<const float4*>(spos), lds, alpha, ns, n_cp, kernel_scale(k),
                                  static_cast<float*>(packed), S(stream)),
                      "fastron_model_pack");
@@ -258,6 +318,7 @@ fastron_status fastron_score_packed(const float* qpos, int64_t nq, int64_t ldq, 
   if (workspace_bytes < need || (need > 0 && !workspace))
     return fail(FASTRON_ERR_WORKSPACE, "fastron_score_packed needs %zu workspace bytes, got %zu", need,
                 workspace_bytes);
+  FASTRON_VALIDATE(vcheck_f32(qpos, n_cp, 4 * nq, 4 * ldq, stream, "qpos"));
   return cuda_status(launch_score(reinterpret_cast<const float4*>(qpos), nq, ldq, static_cast<const float*>(packed), ns,
                                   n_cp, k.kind, kernel_scale(k), score, label, static_cast<double*>(workspace),
                                   S(stream)),
@@ -278,6 +339,7 @@ fastron_status fastron_score_packed_f64(const float* qpos, int64_t nq, int64_t l
   if (workspace_bytes < need || (need > 0 && !workspace))
     return fail(FASTRON_ERR_WORKSPACE, "fastron_score_packed_f64 needs %zu workspace bytes, got %zu", need,
                 workspace_bytes);
+  FASTRON_VALIDATE(vcheck_f32(qpos, n_cp, 4 * nq, 4 * ldq, stream, "qpos"));
   return cuda_status(launch_score(reinterpret_cast<const float4*>(qpos), nq, ldq, static_cast<const float*>(packed), ns,
                                   n_cp, k.kind, kernel_scale(k), nullptr, nullptr, static_cast<double*>(workspace),
                                   S(stream), score64),
@@ -304,6 +366,7 @@ fastron_status fastron_gram(const float* pos, int64_t n, int64_t ldp, int32_t n_
   if (workspace_bytes < need || !workspace)
     return fail(FASTRON_ERR_WORKSPACE, "fastron_gram needs %zu workspace bytes, got %zu", need, workspace_bytes);
   FASTRON_REQUIRE(((uintptr_t)workspace & 255) == 0, "workspace must be 256-byte aligned");
+  FASTRON_VALIDATE(vcheck_f32(pos, n_cp, 4 * n, 4 * ldp, stream, "pos"));
   float* packed = static_cast<float*>(workspace);
   const float c = kernel_scale(k);
   cudaError_t e = launch_pack(reinterpret_cast<const float4*>(pos), ldp, nullptr, n, n_cp, c, packed, S(stream));
@@ -326,6 +389,10 @@ fastron_status fastron_train(const float* K, int64_t n, int64_t ldk, const int8_
   if (n == 0) return cuda_status(cudaMemsetAsync(result, 0, sizeof(*result), S(stream)), "fastron_train");
   FASTRON_REQUIRE(K && y && alpha_inout && F_inout, "K, y, alpha_inout and F_inout must be non-NULL");
   FASTRON_REQUIRE(ldk >= n, "ldk (%lld) < n (%lld)", (long long)ldk, (long long)n);
+  FASTRON_VALIDATE(vcheck_f32(K, n, n, ldk, stream, "K"));
+  FASTRON_VALIDATE(vcheck_labels(y, n, stream));
+  FASTRON_VALIDATE(vcheck_f64(alpha_inout, n, stream, "alpha_inout"));
+  FASTRON_VALIDATE(vcheck_f64(F_inout, n, stream, "F_inout"));
   return cuda_status(launch_train(K, n, ldk, y, beta, iter_max, s_max, alpha_inout, F_inout, support_idx, trace, result,
                                   S(stream)),
                      "fastron_train");
@@ -363,6 +430,10 @@ fastron_status fastron_train_lazy(const float* pos, int64_t n, int64_t ldp, int3
   if (workspace_bytes < need || !workspace)
     return fail(FASTRON_ERR_WORKSPACE, "fastron_train_lazy needs %zu workspace bytes, got %zu", need, workspace_bytes);
   FASTRON_REQUIRE(((uintptr_t)workspace & 255) == 0, "workspace must be 256-byte aligned");
+  FASTRON_VALIDATE(vcheck_f32(pos, n_cp, 4 * n, 4 * ldp, stream, "pos"));
+  FASTRON_VALIDATE(vcheck_labels(y, n, stream));
+  FASTRON_VALIDATE(vcheck_f64(alpha_inout, n, stream, "alpha_inout"));
+  FASTRON_VALIDATE(vcheck_f64(F_inout, n, stream, "F_inout"));
   char* ws = static_cast<char*>(workspace);
   float* packed = reinterpret_cast<float*>(ws);
   float* cache = reinterpret_cast<float*>(ws + align_up(packed_bytes(n, n_cp)));
@@ -442,6 +513,12 @@ fastron_status fastron_edge_check(const fastron_robot* robot, const float* qa, c
     return fail(FASTRON_ERR_WORKSPACE, "fastron_edge_check needs %zu workspace bytes, got %zu", need, workspace_bytes);
   FASTRON_REQUIRE(((uintptr_t)workspace & 255) == 0, "workspace must be 256-byte aligned");
   const int M = robot->n_cp;
+  FASTRON_VALIDATE(vcheck_f32(qa, n_edges, robot->dof, ldq, stream, "qa"));
+  FASTRON_VALIDATE(vcheck_f32(qb, n_edges, robot->dof, ldq, stream, "qb"));
+  if (ns > 0) {
+    FASTRON_VALIDATE(vcheck_f32(spos, M, 4 * ns, 4 * lds, stream, "spos"));
+    FASTRON_VALIDATE(vcheck_f32(alpha, 1, ns, ns, stream, "alpha"));
+  }
   char* ws = static_cast<char*>(workspace);
   float* packed = reinterpret_cast<float*>(ws);
   ws += align_up(packed_bytes(ns, M));
@@ -500,6 +577,11 @@ fastron_status fastron_score_joint(const float* q, int64_t nq, int64_t ldq, cons
   if (workspace_bytes < need || !workspace)
     return fail(FASTRON_ERR_WORKSPACE, "fastron_score_joint needs %zu workspace bytes, got %zu", need, workspace_bytes);
   FASTRON_REQUIRE(((uintptr_t)workspace & 255) == 0, "workspace must be 256-byte aligned");
+  FASTRON_VALIDATE(vcheck_f32(q, nq, dof, ldq, stream, "q"));
+  if (ns > 0) {
+    FASTRON_VALIDATE(vcheck_f32(sx, ns, dof, lds, stream, "s"));
+    FASTRON_VALIDATE(vcheck_f32(alpha, 1, ns, ns, stream, "alpha"));
+  }
   const int Mj = joint_points(dof);
   char* ws = static_cast<char*>(workspace);
   float4* qpts = reinterpret_cast<float4*>(ws);
@@ -537,6 +619,7 @@ fastron_status fastron_gram_joint(const float* x, int64_t n, int64_t ldx, int32_
   if (workspace_bytes < need || !workspace)
     return fail(FASTRON_ERR_WORKSPACE, "fastron_gram_joint needs %zu workspace bytes, got %zu", need, workspace_bytes);
   FASTRON_REQUIRE(((uintptr_t)workspace & 255) == 0, "workspace must be 256-byte aligned");
+  FASTRON_VALIDATE(vcheck_f32(x, n, dof, ldx, stream, "x"));
   const int Mj = joint_points(dof);
   char* ws = static_cast<char*>(workspace);
   float4* pts = reinterpret_cast<float4*>(ws);
@@ -580,6 +663,19 @@ fastron_status fastron_query(const fastron_robot* robot, const float* q, int64_t
     return fail(FASTRON_ERR_WORKSPACE, "fastron_query needs %zu workspace bytes, got %zu", need, workspace_bytes);
   FASTRON_REQUIRE(((uintptr_t)workspace & 255) == 0, "workspace must be 256-byte aligned");
   const bool q_host = is_host_ptr(q), s_host = is_host_ptr(score), l_host = is_host_ptr(label);
+  if (validation_on()) {
+    if (q_host) {
+      for (int64_t i = 0; i < nq; ++i)
+        for (int j = 0; j < D; ++j)
+          FASTRON_REQUIRE(std::isfinite(q[i * ldq + j]), "validation: q[%lld][%d] is not finite", (long long)i, j);
+    } else {
+      FASTRON_VALIDATE(vcheck_f32(q, nq, D, ldq, stream, "q"));
+    }
+    if (ns > 0) {
+      FASTRON_VALIDATE(vcheck_f32(spos, M, 4 * ns, 4 * lds, stream, "spos"));
+      FASTRON_VALIDATE(vcheck_f32(alpha, 1, ns, ns, stream, "alpha"));
+    }
+  }
   const int64_t chunk = nq < kQueryChunk ? nq : kQueryChunk;
   char* ws = static_cast<char*>(workspace);
   float* packed = reinterpret_cast<float*>(ws);

@@ -80,6 +80,12 @@ cudaError_t launch_label_capsules(const float4* pos, int64_t ldp, int64_t n, con
                                   const double* boxes, int n_cubes, float radius, int8_t* label, cudaStream_t st);
 cudaError_t launch_matvec(const float* K, int64_t n, int64_t ldk, const double* alpha, double* F, cudaStream_t st);
 
+// Optional content checks (validate.cu): counts are read back synchronously.
+cudaError_t count_nonfinite(const float* a, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st,
+                            unsigned long long* out);
+cudaError_t count_nonfinite_f64(const double* a, int64_t n, cudaStream_t st, unsigned long long* out);
+cudaError_t count_bad_labels(const int8_t* y, int64_t n, cudaStream_t st, unsigned long long* out);
+
 // K3: Gram
 cudaError_t launch_gram(const float* packed, int64_t n, int M, int kind, float* K, int64_t ldk, cudaStream_t st);
 

@@ -137,3 +137,13 @@ def test_product_package_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src and "liboracle" not in src, f
+
+
+def test_validation_switch():
+    """fastron_set_validation / fastron_validation (include/fastron.h conventions)."""
+    before = fb.validation()
+    fb.set_validation(True)
+    assert fb.validation()
+    fb.set_validation(False)
+    assert not fb.validation()
+    fb.set_validation(before)
