@@ -54,10 +54,17 @@ __host__ __device__ constexpr int gram_cpl(int mp) {  // columns per lane
 }
 
 template <int MP, int KIND, bool JOINT>
-__global__ void __launch_bounds__(kGT) gram_kernel(const float* __restrict__ packed, int64_t n, int M, int m_pow2,
+#ifndef FASTRON_GRAM_RI4
+#define FASTRON_GRAM_RI4 1
+#endif
+#ifndef FASTRON_GRAM_MINB
+#define FASTRON_GRAM_MINB 3
+#endif
+__global__ void __launch_bounds__(kGT, FASTRON_GRAM_MINB) gram_kernel(const float* __restrict__ packed, int64_t n, int M, int m_pow2,
                                                    float inv_m, float* __restrict__ K, int64_t ldk) {
   constexpr int NP = MP / 2;
   constexpr int CPL = gram_cpl(MP);           // columns per lane
+  constexpr int RI = CPL >= 4 ? FASTRON_GRAM_RI4 : kChunkRows;  // rows interleaved per pair loop
   constexpr int WC = 32 * CPL;                // columns per warp
   constexpr int G = kGB / WC;                 // column groups (warps sharing a row range)
   constexpr int R = kGW / G;                  // row groups
@@ -117,14 +124,18 @@ __global__ void __launch_bounds__(kGT) gram_kernel(const float* __restrict__ pac
   // rows past the matrix edge are computed on stale shared memory but never stored
   const int q_end = min(RW, ((rows_here - rbase + kChunkRows - 1) / kChunkRows) * kChunkRows);
   for (int q0 = 0; q0 < q_end; q0 += kChunkRows) {
-    float v[kChunkRows][CPL];  // 8 rows x CPL columns: the chunk, kept for the mirror block
+    float v[kChunkRows][CPL];  // the chunk's rows x CPL columns, kept for the mirror block
+    // pair-major over RI rows at a time: RI x CPL independent accumulation chains per
+    // control-point pair (same per-entry summation order as fastron_score)
+    f2 acc[kChunkRows][CPL];
 #pragma unroll
-    for (int qq = 0; qq < kChunkRows; ++qq) {
-      const int r = rbase + q0 + qq;
-      const float* rec = rows + (r / kTileSupports) * TF + (r % kTileSupports) * NP * 8;
-      f2 acc[CPL];
+    for (int q1 = 0; q1 < kChunkRows; q1 += RI) {
 #pragma unroll
-      for (int p = 0; p < NP; ++p) {
+    for (int p = 0; p < NP; ++p) {
+#pragma unroll
+      for (int qq = q1; qq < q1 + RI; ++qq) {
+        const int r = rbase + q0 + qq;
+        const float* rec = rows + (r / kTileSupports) * TF + (r % kTileSupports) * NP * 8;
         const float4 xy = *reinterpret_cast<const float4*>(rec + p * 8);
         const float2 zz = *reinterpret_cast<const float2*>(rec + p * 8 + 4);
         const f2 vx = pk(xy.x, xy.y), vy = pk(xy.z, xy.w), vz = pk(zz.x, zz.y);
@@ -138,20 +149,24 @@ __global__ void __launch_bounds__(kGT) gram_kernel(const float* __restrict__ pac
 #pragma unroll
         for (int h = 0; h < CPL; ++h) {
           if (JOINT) {  // squared joint-space distance, summed over all pseudo points
-            acc[h] = p == 0 ? mul2(dx[h], dx[h]) : fma2(dx[h], dx[h], acc[h]);
-            acc[h] = fma2(dy[h], dy[h], acc[h]);
-            acc[h] = fma2(dz[h], dz[h], acc[h]);
+            acc[qq][h] = p == 0 ? mul2(dx[h], dx[h]) : fma2(dx[h], dx[h], acc[qq][h]);
+            acc[qq][h] = fma2(dy[h], dy[h], acc[qq][h]);
+            acc[qq][h] = fma2(dz[h], dz[h], acc[qq][h]);
           } else {
             const f2 t = term_from_diffs<KIND>(dx[h], dy[h], dz[h]);
-            acc[h] = p == 0 ? t : add2(acc[h], t);
+            acc[qq][h] = p == 0 ? t : add2(acc[qq][h], t);
           }
         }
       }
+    }
+#pragma unroll
+    for (int qq = q1; qq < q1 + RI; ++qq) {
+      float* Kd = K + (i0 + rbase + q0 + qq) * ldk + c0;
 #pragma unroll
       for (int h = 0; h < CPL; ++h) {
         float x;
         if (JOINT) {
-          const float d2 = pair_sum(acc[h]);
+          const float d2 = pair_sum(acc[qq][h]);
           if (KIND == kGaussian) {
             x = ex2_neg(d2);
           } else {
@@ -159,15 +174,14 @@ __global__ void __launch_bounds__(kGT) gram_kernel(const float* __restrict__ pac
             x = rcp_approx(w * w);
           }
         } else {
-          const float ks = pair_sum(acc[h]);
+          const float ks = pair_sum(acc[qq][h]);
           x = m_pow2 ? ks * inv_m : __fdiv_rn(ks, (float)M);
         }
         v[qq][h] = x;
       }
       // direct block: row i0 + r, the lane's CPL consecutive columns (the warp writes
       // 32*CPL consecutive floats)
-      if (r < rows_here) {
-        float* Kd = K + (i0 + r) * ldk + c0;
+      if (rbase + q0 + qq < rows_here) {
         if (CPL == 4 && vec_ok && cols_full) {
           *reinterpret_cast<float4*>(Kd) = make_float4(v[qq][0], v[qq][CPL > 1 ? 1 : 0], v[qq][CPL > 2 ? 2 : 0],
                                                        v[qq][CPL > 3 ? 3 : 0]);
@@ -179,6 +193,7 @@ __global__ void __launch_bounds__(kGT) gram_kernel(const float* __restrict__ pac
             if (c0 + h < n) Kd[h] = v[qq][h];
         }
       }
+    }
     }
     if (mirror) {
       // mirror block: row c0 + h, columns i0 + rbase + q0 .. +7 (one 32-byte segment)
