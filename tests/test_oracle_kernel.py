@@ -173,3 +173,19 @@ def test_joint_score_and_gram_properties():
     f, lab = oracle.score_joint(oracle.RQ, 1.0, X[:5], X, a)
     np.testing.assert_allclose(f, K[:5] @ a.astype(np.float64), rtol=1e-12, atol=1e-13)
     assert np.array_equal(lab, np.where(f > 0, 1, -1))
+
+
+def test_near_base_points_floor_the_fk_kernel():
+    """Why SURVEY §8(f) f4 (certified early exit / tile culling) cannot pay on these arms
+    (DESIGN.md §11): the first control points stay within ~0.45 m of each other for every
+    configuration, so Eq. 4's mean over M never drops below ~0.14 at gamma = 5, and the
+    remainder of a partial score is bounded only by ~0.14 * sum |alpha_rest|."""
+    robot = W.arm7(8)
+    rng = np.random.default_rng(0)
+    pos = oracle.fk(robot, W.uniform_configs(rng, 400, 7))
+    i, j = rng.integers(0, 400, 5000), rng.integers(0, 400, 5000)
+    k = np.array([oracle.kernel_value(oracle.GAUSSIAN, 5.0, pos[a], pos[b]) for a, b in zip(i, j)])
+    assert k.min() > 0.13
+    # the two base-most points alone give the bound: (1/M) * sum_m exp(-gamma * dmax_m^2)
+    d = np.linalg.norm(pos[i][:, :2] - pos[j][:, :2], axis=-1)
+    assert d.max() < 0.5
