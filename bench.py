@@ -123,10 +123,20 @@ def cpu_baseline(wl, target_s=12.0):
     t64 = run(64)
     nq = int(min(len(wl.queries), max(64, 64 * target_s / max(t64, 1e-6))))
     dt = run(nq)
-    return {"value": nq / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+    cores = oracle.num_threads()
+    # one thread, on a smaller sample (~target_s / 4 of CPU), for the per-core figure
+    oracle.set_num_threads(1)
+    try:
+        t1 = run(16)
+        n1 = int(min(len(wl.queries), max(16, 16 * target_s / 4 / max(t1, 1e-6))))
+        dt1 = run(n1)
+    finally:
+        oracle.set_num_threads(cores)
+    return {"value": nq / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"first {nq} of the {len(wl.queries)} headline queries x all {len(wl.supports)} supports "
                       f"(fp64 FK + score, OpenMP), {dt:.1f} s",
-            "kernel_evals_per_s": nq * len(wl.supports) / dt}
+            "kernel_evals_per_s": nq * len(wl.supports) / dt,
+            "single_thread": {"value": n1 / dt1, "unit": UNIT, "sample": f"first {n1} queries, {dt1:.1f} s"}}
 
 
 def run_reference(args):
@@ -178,6 +188,20 @@ def _time_rows(fb, torch, kind):
         e1.synchronize()
         return e0.elapsed_time(e1) / reps
 
+    def graphed(fn, reps):
+        """The same calls captured once into a CUDA graph and replayed (SURVEY §8(d):
+        separates launch overhead from kernel time)."""
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            fn()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        return timed(g.replay, reps)
+
     # cfg1: 3-DOF, 10k queries x 1k supports, M=4 (launch-latency scale)
     wl = W.score_workload("cfg1")
     spos = fb.fastron_fk(wl.robot, torch.from_numpy(wl.supports).cuda())
@@ -195,8 +219,10 @@ def _time_rows(fb, torch, kind):
         fb.fastron_score_packed(qpos, model, sc, lb, workspace=wsb)
 
     ms = timed(step1, 50)
+    gms = graphed(step1, 50)
     rows["cfg1_score"] = {"ms": ms, "checks_per_s": len(wl.queries) / ms * 1e3,
-                          "kernel_evals_per_s": len(wl.queries) * len(wl.supports) / ms * 1e3}
+                          "kernel_evals_per_s": len(wl.queries) * len(wl.supports) / ms * 1e3,
+                          "graph_replay_ms": gms, "graph_checks_per_s": len(wl.queries) / gms * 1e3}
     # cfg2: 1M x 2k, M=8
     wl = W.score_workload("cfg2")
     spos = fb.fastron_fk(wl.robot, torch.from_numpy(wl.supports).cuda())
@@ -222,9 +248,11 @@ def _time_rows(fb, torch, kind):
     K = torch.empty((len(tw.X), len(tw.X)), device="cuda")
     gws = torch.empty(fb.load_library().fastron_gram_workspace_bytes(len(tw.X), 8), dtype=torch.uint8, device="cuda")
     ms = timed(lambda: fb.fastron_gram(pos, tw.kind, tw.gamma, K=K, workspace=gws), 10)
+    gms = graphed(lambda: fb.fastron_gram(pos, tw.kind, tw.gamma, K=K, workspace=gws), 10)
     n = len(tw.X)
     rows["cfg3_gram"] = {"ms": ms, "unique_pairs": n * (n + 1) // 2,
-                         "mufu_tops": n * n * 8 / 2 / ms * 1e-9, "write_GBps": n * n * 4 / ms * 1e-6}
+                         "mufu_tops": n * n * 8 / 2 / ms * 1e-9, "write_GBps": n * n * 4 / ms * 1e-6,
+                         "graph_replay_ms": gms}
     out = {}
 
     def train():

@@ -72,6 +72,8 @@ def lib():
         L.oracle_gram_joint.restype = None
         L.oracle_num_threads.argtypes = []
         L.oracle_num_threads.restype = ctypes.c_int
+        L.oracle_set_num_threads.argtypes = [ctypes.c_int]
+        L.oracle_set_num_threads.restype = None
         _lib = L
     return _lib
 
@@ -90,6 +92,11 @@ def _robot_arrays(robot):
 
 def num_threads() -> int:
     return int(lib().oracle_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP thread count of the oracle loops (timing only)."""
+    lib().oracle_set_num_threads(int(n))
 
 
 def dh_transform(theta, d, a, alpha) -> np.ndarray:
