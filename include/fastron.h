@@ -274,7 +274,8 @@ fastron_status fastron_gram_joint(const float* x, int64_t n, int64_t ldx, int32_
  *   q: float [nq][ldq], HOST (pageable or pinned) or DEVICE. score (nullable) and
  *   label (nullable): HOST or DEVICE. spos/alpha: device, as fastron_score.
  *   When q / score / label are host memory the call streams them in chunks through the
- *   workspace (H2D of chunk c+1 overlaps compute of chunk c) and returns after the
+ *   workspace (H2D of chunk c+1 and D2H of chunk c-1, on two library-owned copy
+ *   streams, overlap the compute of chunk c on `stream`) and returns after the
  *   results are in host memory (it synchronises `stream`). With device pointers it is
  *   asynchronous like the other calls.
  *   workspace: >= fastron_query_workspace_bytes(nq, ns, robot->n_cp, robot->dof).

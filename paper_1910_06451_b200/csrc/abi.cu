@@ -183,14 +183,16 @@ size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 constexpr int64_t kQueryChunk = 1 << 18;  // queries per pipelined chunk of fastron_query
 
 // One non-blocking copy stream per device for fastron_query's host<->device pipeline.
-cudaStream_t query_copy_stream() {
-  static cudaStream_t streams[64] = {};
+// which = 0: host-to-device copies, 1: device-to-host copies, 2: the second compute stream.
+cudaStream_t query_copy_stream(int which) {
+  static cudaStream_t streams[64][3] = {};
   static std::mutex mu;
   int dev = 0;
   cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
   std::lock_guard<std::mutex> g(mu);
-  if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
-  return streams[dev];
+  if (!streams[dev][which]) cudaStreamCreateWithFlags(&streams[dev][which], cudaStreamNonBlocking);
+  return streams[dev][which];
 }
 
 bool is_host_ptr(const void* p) {
@@ -638,7 +640,7 @@ size_t fastron_query_workspace_bytes(int64_t nq, int64_t ns, int32_t n_cp, int32
   // per in-flight chunk: q (dof floats), positions (n_cp float4), score (float), label (int8); two chunks
   const size_t per = align_up((size_t)chunk * dof * 4) + align_up((size_t)chunk * n_cp * 16) +
                      align_up((size_t)chunk * 4) + align_up((size_t)chunk);
-  return align_up(packed_bytes(ns, n_cp)) + align_up(score_partial_bytes(chunk, ns, n_cp)) + 2 * per;
+  return align_up(packed_bytes(ns, n_cp)) + 2 * align_up(score_partial_bytes(chunk, ns, n_cp)) + 2 * per;
 }
 
 fastron_status fastron_query(const fastron_robot* robot, const float* q, int64_t nq, int64_t ldq, const float* spos,
@@ -680,8 +682,12 @@ fastron_status fastron_query(const fastron_robot* robot, const float* q, int64_t
   char* ws = static_cast<char*>(workspace);
   float* packed = reinterpret_cast<float*>(ws);
   ws += align_up(packed_bytes(ns, M));
-  double* partial = reinterpret_cast<double*>(ws);
-  ws += align_up(score_partial_bytes(chunk, ns, M));
+  double* partials[2];
+  for (int b = 0; b < 2; ++b) {
+    partials[b] = reinterpret_cast<double*>(ws);
+    ws += align_up(score_partial_bytes(chunk, ns, M));
+  }
+  double* partial = partials[0];
   struct Buf { float* q; float* pos; float* sc; int8_t* lb; } buf[2];
   for (int b = 0; b < 2; ++b) {
     buf[b].q = reinterpret_cast<float*>(ws); ws += align_up((size_t)chunk * D * 4);
@@ -707,54 +713,63 @@ fastron_status fastron_query(const fastron_robot* robot, const float* q, int64_t
     }
     return FASTRON_OK;
   }
-  // host buffers: H2D(chunk c+1) on a copy stream overlaps FK+score(chunk c) on `stream`
-  cudaStream_t cp = query_copy_stream();
-  cudaEvent_t ev_in[2], ev_done[2], ev_out[2];
+  // host buffers: H2D(chunk c+1) on one copy stream and D2H(chunk c-1) on another overlap
+  // FK+score(chunk c); chunks alternate between two buffer sets and two compute streams
+  // (`stream` and a library stream), so chunk c+1's kernels fill the SMs that chunk c's
+  // last wave leaves idle, and chunk c+2 reuses chunk c's buffers
+  cudaStream_t h2d = query_copy_stream(0), d2h = query_copy_stream(1);
+  cudaStream_t cs[2] = {st, query_copy_stream(2)};
+  cudaEvent_t ev_in[2], ev_used[2], ev_out[2];
   for (int b = 0; b < 2; ++b) {
     cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev_done[b], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_used[b], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ev_out[b], cudaEventDisableTiming);
+    cudaEventRecord(ev_used[b], st);  // ordered after the model pack and earlier work on `stream`
+    cudaEventRecord(ev_out[b], st);
   }
-  cudaEventRecord(ev_out[0], st);
-  cudaEventRecord(ev_out[1], st);
   int64_t idx = 0;
   for (int64_t off = 0; off < nq && e == cudaSuccess; off += chunk, ++idx) {
     const int b = (int)(idx & 1);
     const int64_t n = nq - off < chunk ? nq - off : chunk;
-    // stage q: the buffer is free once the previous use of it has been copied out
-    cudaStreamWaitEvent(cp, ev_out[b], 0);
+    // stage q once chunk idx-2 (the last user of buffer b) has been computed
     const float* qsrc = q + off * ldq;
     float* qdev = q_host ? buf[b].q : const_cast<float*>(qsrc);
     int64_t ldq_dev = q_host ? D : ldq;
+    cudaStreamWaitEvent(h2d, ev_used[b], 0);
     if (q_host) {
-      if (ldq == D) e = cudaMemcpyAsync(qdev, qsrc, (size_t)n * D * 4, cudaMemcpyHostToDevice, cp);
+      if (ldq == D) e = cudaMemcpyAsync(qdev, qsrc, (size_t)n * D * 4, cudaMemcpyHostToDevice, h2d);
       else e = cudaMemcpy2DAsync(qdev, (size_t)D * 4, qsrc, (size_t)ldq * 4, (size_t)D * 4, (size_t)n,
-                                 cudaMemcpyHostToDevice, cp);
+                                 cudaMemcpyHostToDevice, h2d);
     }
-    cudaEventRecord(ev_in[b], cp);
-    cudaStreamWaitEvent(st, ev_in[b], 0);
+    cudaEventRecord(ev_in[b], h2d);
+    // compute once q is staged and chunk idx-2's results have left buffer b
+    cudaStreamWaitEvent(cs[b], ev_in[b], 0);
+    cudaStreamWaitEvent(cs[b], ev_out[b], 0);
     float* sdev = score ? (s_host ? buf[b].sc : score + off) : nullptr;
     int8_t* ldev = label ? (l_host ? buf[b].lb : label + off) : nullptr;
-    if (e == cudaSuccess) e = launch_fk(P, qdev, n, ldq_dev, reinterpret_cast<float4*>(buf[b].pos), chunk, st);
+    if (e == cudaSuccess) e = launch_fk(P, qdev, n, ldq_dev, reinterpret_cast<float4*>(buf[b].pos), chunk, cs[b]);
     if (e == cudaSuccess)
       e = launch_score(reinterpret_cast<const float4*>(buf[b].pos), n, chunk, packed, ns, M, k.kind, c, sdev, ldev,
-                       partial, st);
-    cudaEventRecord(ev_done[b], st);
-    cudaStreamWaitEvent(cp, ev_done[b], 0);
-    if (e == cudaSuccess && score && s_host) e = cudaMemcpyAsync(score + off, sdev, (size_t)n * 4, cudaMemcpyDeviceToHost, cp);
-    if (e == cudaSuccess && label && l_host) e = cudaMemcpyAsync(label + off, ldev, (size_t)n, cudaMemcpyDeviceToHost, cp);
-    cudaEventRecord(ev_out[b], cp);
-    cudaStreamWaitEvent(st, ev_out[b], 0);
+                       partials[b], cs[b]);
+    cudaEventRecord(ev_used[b], cs[b]);
+    // results out
+    cudaStreamWaitEvent(d2h, ev_used[b], 0);
+    if (e == cudaSuccess && score && s_host) e = cudaMemcpyAsync(score + off, sdev, (size_t)n * 4, cudaMemcpyDeviceToHost, d2h);
+    if (e == cudaSuccess && label && l_host) e = cudaMemcpyAsync(label + off, ldev, (size_t)n, cudaMemcpyDeviceToHost, d2h);
+    cudaEventRecord(ev_out[b], d2h);
   }
-  cudaError_t e2 = cudaStreamSynchronize(cp);
-  cudaError_t e3 = cudaStreamSynchronize(st);
+  cudaStreamWaitEvent(st, ev_used[1], 0);  // `stream` ends after both compute streams
+  cudaError_t e2 = cudaStreamSynchronize(h2d);
+  cudaError_t e3 = cudaStreamSynchronize(d2h);
+  cudaError_t e4 = cudaStreamSynchronize(st);
   for (int b = 0; b < 2; ++b) {
     cudaEventDestroy(ev_in[b]);
-    cudaEventDestroy(ev_done[b]);
+    cudaEventDestroy(ev_used[b]);
     cudaEventDestroy(ev_out[b]);
   }
   if (e == cudaSuccess) e = e2;
   if (e == cudaSuccess) e = e3;
+  if (e == cudaSuccess) e = e4;
   return cuda_status(e, "fastron_query");
 }
 
