@@ -220,10 +220,11 @@ __global__ void __launch_bounds__(kGT, FASTRON_GRAM_MINB) gram_kernel(const floa
 template <int MP, int KIND, bool JOINT = false>
 static cudaError_t run_gram(const float* packed, int64_t n, int M, float* K, int64_t ldk, cudaStream_t st) {
   const size_t smem = 128 + 2 * tile_bytes(MP);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<int> attr[kMaxDevices];
+  const int dev = device_slot();
+  if (!attr[dev].load()) {
     cudaFuncSetAttribute(gram_kernel<MP, KIND, JOINT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+    attr[dev].store(1);
   }
   const int64_t nb = (n + kGB - 1) / kGB;
   const int64_t tiles = nb * (nb + 1) / 2;

@@ -19,6 +19,14 @@ struct DeviceInfo {
 };
 const DeviceInfo& device_info();
 
+// Function attributes and occupancy are per device: kernels keep one cached value per
+// device ordinal (0 = not yet computed).
+constexpr int kMaxDevices = 64;
+inline int device_slot() {
+  const int d = device_info().device;
+  return d >= 0 && d < kMaxDevices ? d : 0;
+}
+
 // K1: control-point positions, float4 [M][ldpos]
 cudaError_t launch_fk(const FkParams& P, const float* q, int64_t n, int64_t ldq, float4* pos, int64_t ldpos,
                       cudaStream_t st);

@@ -393,15 +393,18 @@ size_t score_partial_bytes(int64_t nq, int64_t ns, int M) {
 
 template <int MP, int KIND, int MODE>
 static int score_ctas_per_sm() {
-  static int cached = -1;
-  if (cached < 0) {
+  static std::atomic<int> cached[kMaxDevices];
+  const int dev = device_slot();
+  int v = cached[dev].load();
+  if (v == 0) {
     const size_t smem = 128 + kStages * tile_bytes(MP);
     int n = 0;
     cudaFuncSetAttribute(score_kernel<MP, KIND, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, score_kernel<MP, KIND, MODE>, kNT, smem);
-    cached = n > 0 ? n : 1;
+    v = n > 0 ? n : 1;
+    cached[dev].store(v);
   }
-  return cached;
+  return v;
 }
 
 static ScorePlan make_plan(int64_t nq, int64_t ns, int M, int ctas_per_sm) {

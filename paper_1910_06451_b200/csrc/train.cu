@@ -542,11 +542,12 @@ int64_t train_max_n() { return kChunkMax * kMaxCluster; }
 
 template <int EPT, int LMP = 0, int LKIND = 0>
 static cudaError_t launch_ept(const TrainArgs& A, int C, cudaStream_t st, size_t smem) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<int> attr[kMaxDevices];
+  const int dev = device_slot();
+  if (!attr[dev].load()) {
     cudaFuncSetAttribute(train_kernel<EPT, LMP, LKIND>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(train_kernel<EPT, LMP, LKIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    attr = true;
+    attr[dev].store(1);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C, 1, 1);
