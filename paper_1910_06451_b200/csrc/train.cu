@@ -598,9 +598,12 @@ cudaError_t launch_train(const float* K, int64_t n, int64_t ldk, const int8_t* y
   const int64_t ept = (A.chunk + kTrainNT - 1) / kTrainNT;
   const size_t smem = (size_t)A.chunk * 8;
   cudaError_t e;
+  // the smallest instance that covers the slice: dead slots still cost a load and an update
   if (ept <= 2) e = launch_ept<2>(A, C, st, smem);
   else if (ept <= 4) e = launch_ept<4>(A, C, st, smem);
+  else if (ept <= 6) e = launch_ept<6>(A, C, st, smem);
   else if (ept <= 8) e = launch_ept<8>(A, C, st, smem);
+  else if (ept <= 10) e = launch_ept<10>(A, C, st, smem);
   else e = launch_ept<12>(A, C, st, smem);
   g_launches.fetch_add(1);
   return e;
