@@ -61,12 +61,19 @@ def test_claim2_loss_decrease_and_invariants(seed):
             F = K @ alpha
             margin_before = y[i] * F[i]
             assert margin_before <= 0
+            # Alg. 1 line "i = argmin y F": no margin is smaller (up to the
+            # rounding difference between the oracle's incremental F and K @ alpha)
+            assert margin_before <= (y * F).min() + 1e-12
             alpha[i] += b[i] * y[i] - F[i]
             assert y[i] * (K @ alpha)[i] == pytest.approx(b[i], abs=1e-9)
             assert L[t + 1] - L[t] <= -0.5 + 1e-9
             assert L[t + 1] - L[t] == pytest.approx(-0.5 * (b[i] - margin_before) ** 2, abs=1e-8)
         else:
             i = -code - 1
+            # removal candidate: argmax over alpha != 0 of y (F - alpha), > 0
+            F = K @ alpha
+            red = np.where(alpha != 0, y * (F - alpha), -np.inf)
+            assert alpha[i] != 0 and red[i] >= red.max() - 1e-12 and red[i] > 0
             alpha[i] = 0.0
             assert y[i] * (K @ alpha)[i] > -1e-12
         assert np.all(y * alpha >= 0)
