@@ -47,10 +47,11 @@ def _check(robot, qa, qb, n_interp, sup, alpha, kind, gamma):
     return hit, ref_hit, fmax
 
 
-def test_cfg4_subset():
+@pytest.mark.parametrize("kind", [W.GAUSSIAN, W.RQ])
+def test_cfg4_subset(kind):
     require_gpu()
-    wl = W.edge_workload(n_edges=1500)
-    hit, ref, fmax = _check(wl.robot, wl.qa, wl.qb, wl.n_interp, wl.supports, wl.alpha, 0, wl.gamma)
+    wl = W.edge_workload(n_edges=1500, kind=kind)
+    hit, ref, fmax = _check(wl.robot, wl.qa, wl.qb, wl.n_interp, wl.supports, wl.alpha, kind, wl.gamma)
     assert 0 < hit.sum() < len(hit)
 
 

@@ -6,7 +6,7 @@ import pytest
 
 import oracle
 import workloads as W
-from gpu_helpers import assert_score_parity, dev, require_gpu, soa_from_oracle
+from gpu_helpers import assert_score_parity, dev, require_gpu, rq_floor, soa_from_oracle
 
 pytestmark = pytest.mark.gpu
 
@@ -52,17 +52,19 @@ def test_cfg5_subset_m16():
     assert_score_parity(s, f, l, what="cfg5 M=16")
 
 
-def test_headline_full_size_sampled():
+@pytest.mark.parametrize("kind", [W.GAUSSIAN, W.RQ])
+def test_headline_full_size_sampled(kind):
     """Headline size (1M queries x 20k supports, the bench launch configuration):
     the oracle recomputes a seeded sample of 1,000 queries plus the 500 GPU scores
-    nearest zero (the label boundary)."""
+    nearest zero (the label boundary). Gaussian is the headline term; RQ is Eq. 3."""
     require_gpu()
-    wl = W.score_workload("headline")
-    s, l = _gpu_scores(wl.robot, wl.supports, wl.alpha, wl.queries, 0, wl.gamma)
+    wl = W.score_workload("headline", kind=kind)
+    s, l = _gpu_scores(wl.robot, wl.supports, wl.alpha, wl.queries, kind, wl.gamma)
     rng = np.random.default_rng(0)
     idx = np.unique(np.concatenate([rng.choice(len(s), 1000, replace=False), np.argsort(np.abs(s))[:500]]))
-    f, _ = _ref_scores(wl.robot, wl.supports, wl.alpha, wl.queries[idx], 0, wl.gamma)
-    assert_score_parity(s[idx], f, l[idx], what="headline sample")
+    f, _ = _ref_scores(wl.robot, wl.supports, wl.alpha, wl.queries[idx], kind, wl.gamma)
+    floor = 1e-5 if kind == W.GAUSSIAN else rq_floor(len(wl.supports))  # R16 / R24
+    assert_score_parity(s[idx], f, l[idx], floor=floor, what=f"headline sample kind={kind}")
 
 
 @pytest.mark.parametrize("M", [1, 3, 5, 32])
