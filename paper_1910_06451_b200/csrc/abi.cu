@@ -489,7 +489,8 @@ fastron_status fastron_kernel_matvec(const float* K, int64_t n, int64_t ldk, con
 size_t fastron_edge_workspace_bytes(int64_t n_edges, int64_t ns, int32_t n_cp) {
   if (n_edges < 0 || ns < 0 || n_cp < 1 || n_cp > FASTRON_MAX_CP) return 0;
   const size_t lists = 2 * align_up((size_t)n_edges * 4) + 256;  // two active lists + two counters
-  return align_up(packed_bytes(ns, n_cp)) + align_up(score_partial_bytes(n_edges * 32, ns, n_cp)) + lists;
+  const size_t pos = align_up((size_t)n_edges * 32 * n_cp * 16);  // a round's control points
+  return align_up(packed_bytes(ns, n_cp)) + align_up(score_partial_bytes(n_edges * 32, ns, n_cp)) + lists + pos;
 }
 
 fastron_status fastron_edge_check(const fastron_robot* robot, const float* qa, const float* qb, int64_t n_edges,
@@ -529,6 +530,8 @@ fastron_status fastron_edge_check(const fastron_robot* robot, const float* qa, c
   int32_t* counts = reinterpret_cast<int32_t*>(ws);  // [2] live counters (256 B reserved)
   ws += 256;
   int32_t* lists[2] = {reinterpret_cast<int32_t*>(ws), reinterpret_cast<int32_t*>(ws + align_up((size_t)n_edges * 4))};
+  ws += 2 * align_up((size_t)n_edges * 4);
+  float4* epos = reinterpret_cast<float4*>(ws);
   const float c = kernel_scale(k);
   cudaStream_t st = S(stream);
   cudaError_t e = launch_pack(reinterpret_cast<const float4*>(spos), lds, alpha, ns, M, c, packed, st);
@@ -551,7 +554,7 @@ fastron_status fastron_edge_check(const fastron_robot* robot, const float* qa, c
     R.hit_index = hit_index;
     e = cudaMemsetAsync(R.next_count, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return cuda_status(e, "fastron_edge_check(memset)");
-    e = launch_edge_round(P, R, packed, ns, M, k.kind, c, partial, st);
+    e = launch_edge_round(P, R, packed, ns, M, k.kind, c, partial, epos, st);
     if (e != cudaSuccess) return cuda_status(e, "fastron_edge_check");
   }
   return FASTRON_OK;

@@ -69,8 +69,9 @@ struct EdgeRound {
   uint8_t* in_collision;
   int32_t* hit_index;
 };
+// pos: workspace for the round's control points, float4 [M][32 * n_edges]
 cudaError_t launch_edge_round(const FkParams& P, const EdgeRound& R, const float* packed, int64_t ns, int M, int kind,
-                              float scale, double* partial, cudaStream_t st);
+                              float scale, double* partial, float4* pos, cudaStream_t st);
 
 // Joint-space RBF baseline ("Fastron RBF"): joint vectors as zero-padded pseudo points.
 int joint_points(int D);

@@ -152,6 +152,37 @@ __device__ __forceinline__ void edge_vote(const ScoreArgs& A, int64_t vq, double
   }
 }
 
+// K4 prologue, once per round: virtual query vq = (active slot vq / 32, lane vq % 32) ->
+// interpolated configuration q_k = qa + t_k (qb - qa) in fp32 (R11) -> fp64 FK chain ->
+// fp32 control points, SoA float4 [M][nq] (the layout the score kernel reads). Lanes past
+// n_interp get zeros (they never vote). Computed once instead of in every support split.
+__global__ void __launch_bounds__(256) edge_fk_kernel(const __grid_constant__ ScoreArgs A,
+                                                      const __grid_constant__ FkParams P, float4* __restrict__ pos) {
+  const int64_t vq = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (vq >= edge_active_queries(A)) return;
+  const int64_t slot = vq >> 5;
+  const int o = A.round * 32 + (int)(vq & 31);
+  if (o >= A.n_interp) {
+    for (int m = 0; m < A.M; ++m) pos[(int64_t)m * A.nq + vq] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  const int32_t e = A.active ? A.active[slot] : (int32_t)slot;
+  const int k = edge_point(A.n_interp, o);
+  const float t = A.n_interp > 1 ? __fdiv_rn((float)k, (float)(A.n_interp - 1)) : 0.0f;
+  const float* qa = A.qa + (int64_t)e * A.ldqe;
+  const float* qb = A.qb + (int64_t)e * A.ldqe;
+  fk_chain(
+      P,
+      [&](int jj) {
+        const float a = __ldg(qa + jj), b = __ldg(qb + jj);
+        return (double)__fadd_rn(a, __fmul_rn(t, __fsub_rn(b, a)));
+      },
+      [&](int m, double x, double y, double z) {
+        pos[(int64_t)m * A.nq + vq] =
+            make_float4(__double2float_rn(x), __double2float_rn(y), __double2float_rn(z), 0.0f);
+      });
+}
+
 template <int MP, int KIND, int MODE>
 __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ ScoreArgs A,
                                                     const __grid_constant__ FkParams P) {
@@ -195,40 +226,15 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
     float px[MP], py[MP], pz[MP];
 #pragma unroll
     for (int m = 0; m < MP; ++m) px[m] = py[m] = pz[m] = 0.0f;
-    if (MODE == MODE_POS || MODE == MODE_JOINT) {
-      if (vq < A.nq) {
+    // positions of the query (MODE_EDGE: of the interpolated configuration, written by
+    // edge_fk_kernel for this round)
+    if (vq < nq_live) {
 #pragma unroll
-        for (int m = 0; m < MP; ++m) {
-          if (m < A.M) {
-            const float4 v = __ldg(A.qpos + (int64_t)m * A.ldq + vq);
-            px[m] = v.x; py[m] = v.y; pz[m] = v.z;
-          }
+      for (int m = 0; m < MP; ++m) {
+        if (m < A.M) {
+          const float4 v = __ldg(A.qpos + (int64_t)m * A.ldq + vq);
+          px[m] = v.x; py[m] = v.y; pz[m] = v.z;
         }
-      }
-    } else {
-      const int64_t slot = vq >> 5;
-      const int o = A.round * 32 + (int)(vq & 31);
-      if (vq < nq_live && o < A.n_interp) {
-        const int32_t e = A.active ? A.active[slot] : (int32_t)slot;
-        const int k = edge_point(A.n_interp, o);
-        const float t = A.n_interp > 1 ? __fdiv_rn((float)k, (float)(A.n_interp - 1)) : 0.0f;
-        const float* qa = A.qa + (int64_t)e * A.ldqe;
-        const float* qb2 = A.qb + (int64_t)e * A.ldqe;
-        float tmp[MP][3];
-        fk_chain(
-            P,
-            [&](int jj) {
-              const float a = __ldg(qa + jj), b = __ldg(qb2 + jj);
-              return (double)__fadd_rn(a, __fmul_rn(t, __fsub_rn(b, a)));
-            },
-            [&](int m, double x, double y, double z) {
-              tmp[m][0] = __double2float_rn(x);
-              tmp[m][1] = __double2float_rn(y);
-              tmp[m][2] = __double2float_rn(z);
-            });
-#pragma unroll
-        for (int m = 0; m < MP; ++m)
-          if (m < A.M) { px[m] = tmp[m][0]; py[m] = tmp[m][1]; pz[m] = tmp[m][2]; }
       }
     }
 #pragma unroll
@@ -560,10 +566,12 @@ cudaError_t launch_score(const float4* qpos, int64_t nq, int64_t ldq, const floa
 }
 
 cudaError_t launch_edge_round(const FkParams& P, const EdgeRound& R, const float* packed, int64_t ns, int M, int kind,
-                              float scale, double* partial, cudaStream_t st) {
+                              float scale, double* partial, float4* pos, cudaStream_t st) {
   if (R.n_edges <= 0) return cudaSuccess;
   ScoreArgs A = {};
   A.nq = R.n_edges * 32;
+  A.qpos = pos;
+  A.ldq = A.nq;
   A.packed = packed;
   A.M = M;
   A.scale = scale;
@@ -580,6 +588,10 @@ cudaError_t launch_edge_round(const FkParams& P, const EdgeRound& R, const float
   A.in_collision = R.in_collision;
   A.hit_index = R.hit_index;
   A.denom = (double)M;
+  edge_fk_kernel<<<(unsigned)((A.nq + 255) / 256), 256, 0, st>>>(A, P, pos);
+  g_launches.fetch_add(1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
   return dispatch<MODE_EDGE>(A, P, A.nq, ns, kind, st);
 }
 
