@@ -47,7 +47,6 @@ struct ScorePlan {
 };
 int score_queries_per_cta(int M);
 int score_max_splits(int64_t nq, int64_t ns, int M);
-ScorePlan plan_score(int64_t nq, int64_t ns, int M, int kind);
 size_t score_partial_bytes(int64_t nq, int64_t ns, int M);
 
 cudaError_t launch_score(const float4* qpos, int64_t nq, int64_t ldq, const float* packed, int64_t ns, int M, int kind,

@@ -540,11 +540,6 @@ cudaError_t launch_score_joint(const float4* qpts, int64_t nq, const float* pack
   }
 }
 
-ScorePlan plan_score(int64_t nq, int64_t ns, int M, int kind) {
-  (void)kind;
-  return make_plan(nq, ns, M, 3);
-}
-
 cudaError_t launch_score(const float4* qpos, int64_t nq, int64_t ldq, const float* packed, int64_t ns, int M, int kind,
                          float scale, float* score, int8_t* label, double* partial, cudaStream_t st,
                          double* score64) {

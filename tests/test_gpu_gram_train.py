@@ -8,7 +8,7 @@ import pytest
 
 import oracle
 import workloads as W
-from gpu_helpers import assert_score_parity, dev, positions_np, require_gpu
+from gpu_helpers import assert_score_parity, dev, require_gpu
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")

@@ -2,7 +2,7 @@
 line (FASTRON_LIB selects the library build)."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np, torch
+import torch
 import paper_1910_06451_b200 as fb, workloads as W
 ew = W.edge_workload(kind=int(os.environ.get("KIND", "0")))
 spos = fb.fastron_fk(ew.robot, torch.from_numpy(ew.supports).cuda())

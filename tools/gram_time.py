@@ -1,7 +1,7 @@
 """Time fastron_gram on cfg3 (N=5000, M=8) and a 20k M=16 case (cfg5 size); one JSON line."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np, torch
+import torch
 import paper_1910_06451_b200 as fb, workloads as W
 out = {"lib": os.environ.get("FASTRON_LIB", "default")}
 for name, (robot, X) in {"cfg3": (W.train_workload().robot, W.train_workload().X),
