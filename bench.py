@@ -394,9 +394,15 @@ def run_ours(args):
     robot = fb.make_robot_struct(wl.robot)
     st = torch.cuda.current_stream()
 
-    # model (support set): FK + pack once per model update
+    # model (support set): FK + pack once per model update, on rank 0; replicated to the
+    # other ranks by one broadcast of the packed buffer, outside the timed region
     spos = fb.fastron_fk(robot, torch.from_numpy(wl.supports).cuda())
     model = fb.fastron_model_pack(spos, torch.from_numpy(wl.alpha).cuda(), wl.kind, wl.gamma)
+    if ws > 1:
+        if rank != 0:
+            model.buf.zero_()
+        fd.broadcast_model(model.buf, src=0)
+        torch.cuda.synchronize()
     q = torch.from_numpy(queries).cuda()
     qpos = torch.empty((M, Q, 4), device="cuda")
     score = torch.empty(Q, device="cuda")

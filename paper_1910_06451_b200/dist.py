@@ -1,7 +1,8 @@
 """Host-side multi-GPU plumbing for the query-sharded (weak-scaling) bench path.
 
 Queries are independent units: every rank scores its own batch against
-a replicated model, so the data path has no collective. The only collectives are the
+a replicated model, so the data path has no collective. The collectives are the model
+replication after a model update (one broadcast of the packed model), the
 timing barrier and the max-over-ranks reduction of the measured time.
 Works with the nccl (GPU) and gloo (CPU tests) backends.
 """
@@ -25,6 +26,23 @@ def shard_queries(base_queries: np.ndarray, rank: int, seed: int = 1000) -> np.n
         return base_queries
     rng = np.random.default_rng(seed + rank)
     return rng.uniform(-np.pi, np.pi, size=base_queries.shape).astype(np.float32)
+
+
+def shard_range(n: int, rank: int, world_size: int) -> tuple:
+    """Contiguous partition of n independent units (queries or edges) over the ranks, for a
+    fixed total batch (strong scaling): rank r gets [lo, hi); sizes differ by at most 1."""
+    base, extra = divmod(int(n), int(world_size))
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def broadcast_model(packed, src: int = 0):
+    """Replicate a packed model (fastron_model_pack output, a flat tensor) from rank `src`
+    to every rank in place — one broadcast per model update (no-op on a single process)."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.broadcast(packed, src=src)
+    return packed
 
 
 def max_over_ranks(value: float, device=None) -> float:

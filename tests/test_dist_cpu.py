@@ -29,7 +29,13 @@ def _worker(rank, world, port, out):
     q = fd.shard_queries(base, r)
     local_ms = 10.0 + 5.0 * r  # rank 1 is the slow one
     mx = fd.max_over_ranks(local_ms)
-    out[rank] = (ws, r, float(q[0, 0]), float(q.mean()), mx, fd.aggregate_rate(len(q), ws, mx))
+    # model replication: rank 0's packed model overwrites every other rank's buffer
+    import torch
+    model = torch.full((1000,), float(r + 1), dtype=torch.float32) if r == 0 else torch.zeros(1000)
+    fd.broadcast_model(model, src=0)
+    lo, hi = fd.shard_range(1001, r, ws)
+    out[rank] = (ws, r, float(q[0, 0]), float(q.mean()), mx, fd.aggregate_rate(len(q), ws, mx),
+                 float(model.sum()), (lo, hi))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -47,6 +53,19 @@ def test_two_rank_gloo_sharding_and_timing():
     assert abs(r0[3]) < 0.2 and abs(r1[3]) < 0.2  # same U[-pi, pi] distribution
     assert r0[4] == r1[4] == 15.0  # max over ranks, seen identically everywhere
     assert r0[5] == r1[5] == pytest.approx(2 * 1000 / 15e-3)
+    assert r0[6] == r1[6] == 1000.0  # the broadcast model is rank 0's everywhere
+    assert r0[7] == (0, 501) and r1[7] == (501, 1001)  # contiguous shards cover the batch
+
+
+def test_shard_range_partitions():
+    from paper_1910_06451_b200 import dist as fd
+    for n in (0, 1, 7, 1000, 1001):
+        for ws in (1, 2, 3, 8):
+            parts = [fd.shard_range(n, r, ws) for r in range(ws)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            assert all(parts[i][1] == parts[i + 1][0] for i in range(ws - 1))
+            sizes = [hi - lo for lo, hi in parts]
+            assert max(sizes) - min(sizes) <= 1
 
 
 def test_single_process_defaults():
