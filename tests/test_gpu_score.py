@@ -166,6 +166,16 @@ def test_query_host_pipeline_matches_device_path():
     fb.fastron_query(wl.robot, dev(wl.queries[:1000]), spos, alpha, 0, wl.gamma, score=sd)
     torch.cuda.synchronize()
     assert np.array_equal(sd.cpu().numpy(), s_dev[:1000])
+    # mixed: host q (3 chunks, the last ragged), device scores, host labels only
+    n3 = 2 * 262_144 + 17
+    sd3 = torch.empty(n3, dtype=torch.float32, device="cuda")
+    lh3 = torch.empty(n3, dtype=torch.int8).pin_memory()
+    fb.fastron_query(wl.robot, qh[:n3], spos, alpha, 0, wl.gamma, score=sd3, label=lh3)
+    torch.cuda.synchronize()
+    assert np.array_equal(sd3.cpu().numpy(), s_dev[:n3]) and np.array_equal(lh3.numpy(), l_dev[:n3])
+    lh4 = torch.empty(n3, dtype=torch.int8).pin_memory()
+    fb.fastron_query(wl.robot, qh[:n3], spos, alpha, 0, wl.gamma, score=None, label=lh4)
+    assert np.array_equal(lh4.numpy(), l_dev[:n3])
 
 
 def test_cfg5_full_size_sampled():
