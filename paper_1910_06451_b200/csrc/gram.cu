@@ -2,17 +2,20 @@
 // Algorithm 1's "computeKernelMatrixColumn").
 //
 // Upper-triangular 128x128 tiles (bi <= bj), one CTA of 4 warps per tile:
-//  * COLUMN points live in registers: each lane holds CPL consecutive columns (4 at
-//    M <= 8, 2 at M <= 16) as pre-scaled f32x2 control-point pairs (the packed records of
+//  * COLUMN points live in registers: each lane holds CPL consecutive columns (2 at
+//    M <= 16, 1 above) as pre-scaled f32x2 control-point pairs (the packed records of
 //    the scoring kernel); a warp covers 32*CPL columns;
 //  * the tile's 128 ROW points arrive as two packed support tiles by one TMA bulk copy;
 //    each warp walks a contiguous row range; a row record is a warp-broadcast
 //    LDS.128 + LDS.64 shared by the lane's CPL columns;
 //  * the (bi, bj) block is stored straight from registers: for a fixed row each lane
 //    writes its CPL consecutive floats as one vector store (the warp covers 32*CPL
-//    consecutive floats). The lane keeps its last 8 rows x CPL values in registers and
-//    writes the mirrored (bj, bi) block from them: one 32-byte segment (two float4) per
-//    column per 8 rows — no shared-memory transpose, one store per row per lane.
+//    consecutive floats). The lane keeps its last 4 rows x CPL values in registers and
+//    writes the mirrored (bj, bi) block from them: one 16-byte segment per column per 4
+//    rows — no shared-memory transpose, about one store per row per lane;
+//  * the 4 rows of a chunk are processed pair-major (each control-point pair for all 4
+//    rows x CPL columns): 4*CPL independent chains instead of one row's dependency tail;
+//  * __launch_bounds__ asks for 4 resident CTAs at M <= 8 and 3 above.
 // JOINT = true builds the joint-space RBF Gram of the "Fastron RBF" baseline (PAPER.md:37,
 // :114-117) from zero-padded pseudo points: one RBF term of the whole squared distance.
 // The same term_pair() and control-point summation order as fastron_score make K_ij
@@ -28,7 +31,7 @@ namespace fastron {
 #define FASTRON_GRAM_WARPS 4
 #endif
 #ifndef FASTRON_GRAM_CPL8
-#define FASTRON_GRAM_CPL8 4
+#define FASTRON_GRAM_CPL8 2
 #endif
 constexpr int kGT = 32 * FASTRON_GRAM_WARPS;  // threads per Gram CTA
 constexpr int kGW = kGT / 32;
@@ -49,19 +52,21 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t nb, int64_t& bi, 
   bj = r + (t - start(r));
 }
 
+#ifndef FASTRON_GRAM_RI4
+#define FASTRON_GRAM_RI4 1
+#endif
+
 __host__ __device__ constexpr int gram_cpl(int mp) {  // columns per lane
   return mp <= 8 ? FASTRON_GRAM_CPL8 : mp <= 16 ? (FASTRON_GRAM_CPL8 < 2 ? FASTRON_GRAM_CPL8 : 2) : 1;
 }
 
+// resident CTAs per SM the register allocation must allow: 4 at M <= 8, 3 above
+__host__ __device__ constexpr int gram_min_blocks(int mp) { return mp <= 8 ? 4 : 3; }
+
 template <int MP, int KIND, bool JOINT>
-#ifndef FASTRON_GRAM_RI4
-#define FASTRON_GRAM_RI4 1
-#endif
-#ifndef FASTRON_GRAM_MINB
-#define FASTRON_GRAM_MINB 3
-#endif
-__global__ void __launch_bounds__(kGT, FASTRON_GRAM_MINB) gram_kernel(const float* __restrict__ packed, int64_t n, int M, int m_pow2,
-                                                   float inv_m, float* __restrict__ K, int64_t ldk) {
+__global__ void __launch_bounds__(kGT, gram_min_blocks(MP))
+    gram_kernel(const float* __restrict__ packed, int64_t n, int M, int m_pow2, float inv_m, float* __restrict__ K,
+                int64_t ldk) {
   constexpr int NP = MP / 2;
   constexpr int CPL = gram_cpl(MP);           // columns per lane
   constexpr int RI = CPL >= 4 ? FASTRON_GRAM_RI4 : kChunkRows;  // rows interleaved per pair loop
