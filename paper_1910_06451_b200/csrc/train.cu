@@ -149,6 +149,25 @@ __device__ __forceinline__ Cand warp_best(const Cand& c) {
   return b;
 }
 
+// The lane holding the warp's lexicographic best (key, idx) — warp_argbest without
+// distributing the winner (its owner already has it). -1: every lane empty.
+template <bool MAX_KEY>
+__device__ __forceinline__ int warp_arglane(uint64_t key, int idx) {
+  const unsigned full = 0xffffffffu;
+  const bool live = idx != kNone;
+  const uint32_t h = (uint32_t)(key >> 32), l = (uint32_t)key;
+  const uint32_t bh = MAX_KEY ? __reduce_max_sync(full, live ? h : 0u) : __reduce_min_sync(full, live ? h : 0xffffffffu);
+  const unsigned hmask = __ballot_sync(full, live && h == bh);
+  if (hmask == 0u) return -1;
+  if (__popc(hmask) == 1) return __ffs(hmask) - 1;
+  const uint32_t bl = MAX_KEY ? __reduce_max_sync(full, (live && h == bh) ? l : 0u)
+                              : __reduce_min_sync(full, (live && h == bh) ? l : 0xffffffffu);
+  const bool eq = live && h == bh && l == bl;
+  const int bidx = (int)__reduce_min_sync(full, eq ? (unsigned)idx : (unsigned)kNone);
+  const unsigned own = __ballot_sync(full, eq && idx == bidx);
+  return own ? __ffs(own) - 1 : -1;
+}
+
 __device__ __forceinline__ float ld_evict_last(const float* p, uint64_t pol) {
   float v;
   asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
@@ -368,15 +387,13 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
     if (m1 < m0 || (m1 == m0 && k1 >= 0 && k1 < k0)) { mk = m1; mkk = k1; }
     const int my_idx = (mkk >= 0 && mk != INFINITY) ? lo + mkk * kTrainNT + tid : kNone;
     {
-      uint64_t wkey;
-      int widx;
       const uint64_t okey = order_key(mk);
       PROF_MARK(6);
-      const int wl = warp_argbest<false>(okey, my_idx, wkey, widx);
+      const int wl = warp_arglane<false>(okey, my_idx);
       PROF_MARK(7);
-      if (lane == wl) {  // the owner lane attaches the payload of the warp winner
+      if (lane == wl) {  // the owner lane writes the warp winner with its payload
         const int jw = mkk * kTrainNT + tid;
-        s_warp[parity][warp] = Cand{wkey, mk, s_Y[jw], widx, ((yneg >> mkk) & 1u) ? -1 : 1, LAZY ? s_slot[jw] : -1, 0};
+        s_warp[parity][warp] = Cand{okey, mk, s_Y[jw], my_idx, ((yneg >> mkk) & 1u) ? -1 : 1, LAZY ? s_slot[jw] : -1, 0};
       } else if (wl < 0 && lane == 0) {
         s_warp[parity][warp] = cand_none(false);
       }
@@ -420,12 +437,11 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
       }
       const int ridx = rkk >= 0 ? lo + rkk * kTrainNT + tid : kNone;
       {
-        uint64_t wkey;
-        int widx;
-        const int wl = warp_argbest<true>(order_key(rk), ridx, wkey, widx);
+        const uint64_t rkey = order_key(rk);
+        const int wl = warp_arglane<true>(rkey, ridx);
         if (lane == wl) {
           const int jw = rkk * kTrainNT + tid;
-          s_warp[q][warp] = Cand{wkey, 0.0, s_Y[jw], widx, ((yneg >> rkk) & 1u) ? -1 : 1, LAZY ? s_slot[jw] : -1, 0};
+          s_warp[q][warp] = Cand{rkey, 0.0, s_Y[jw], ridx, ((yneg >> rkk) & 1u) ? -1 : 1, LAZY ? s_slot[jw] : -1, 0};
         } else if (wl < 0 && lane == 0) {
           s_warp[q][warp] = cand_none(true);
         }
