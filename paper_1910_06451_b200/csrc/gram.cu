@@ -116,6 +116,14 @@ __global__ void __launch_bounds__(kGT, gram_min_blocks(MP))
       uy[h][p] = pk(xy.z, xy.w);
       uz[h][p] = pk(zz.x, zz.y);
     }
+    // odd M: the packed records pad control point MP-1 with a far value; on the column
+    // side it becomes 0 (as a scoring query's), so padded - pad is far and the term is
+    // exactly 0 — not 1, which pad - pad would give
+    if (!JOINT && M < MP) {
+      ux[h][NP - 1] = pk(lo(ux[h][NP - 1]), 0.0f);
+      uy[h][NP - 1] = pk(lo(uy[h][NP - 1]), 0.0f);
+      uz[h][NP - 1] = pk(lo(uz[h][NP - 1]), 0.0f);
+    }
   }
   mbar_wait(bar, 0);
 

@@ -346,6 +346,11 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
           vy[p] = pk(xy.z, xy.w);
           vz[p] = pk(zz.x, zz.y);
         }
+        if (A.M < LMP) {  // odd M: x_i's padded point at 0 so the padded term is 0 (as in K3)
+          vx[LNP - 1] &= 0xffffffffull;  // high lane (control point MP-1) := +0.0f
+          vy[LNP - 1] &= 0xffffffffull;
+          vz[LNP - 1] &= 0xffffffffull;
+        }
 #pragma unroll
         for (int k = 0; k < EPT; ++k) {
           const float* rec = s_rec + (int64_t)koff[k] * LNP * 8;

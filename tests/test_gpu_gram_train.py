@@ -53,6 +53,23 @@ def test_gram_m16_and_ldk():
     assert_score_parity(Kh[:, :400].ravel(), Kr.ravel(), what="gram M=16")
 
 
+@pytest.mark.parametrize("M", [1, 3, 5, 12, 32])
+def test_gram_odd_and_extreme_m(M):
+    """Every column-per-lane path (CPL 2 at M <= 16, 1 above), padded control points of odd
+    M, and the non-power-of-two 1/M division: parity, exact symmetry, unit diagonal."""
+    require_gpu()
+    base = W.arm7(8)
+    rng = np.random.default_rng(100 + M)
+    robot = W.make_robot("m%d" % M, base.dh, rng.integers(0, 8, size=M), rng.uniform(-0.1, 0.1, size=(M, 3)))
+    X = rng.uniform(-np.pi, np.pi, size=(301, 7)).astype(np.float32)
+    for kind in (0, 1):
+        _, K = _gram(robot, X, kind, 5.0)
+        Kg = K.cpu().numpy()
+        assert np.array_equal(Kg, Kg.T) and np.all(np.diag(Kg) == 1.0)
+        Kr = oracle.gram(kind, 5.0, oracle.fk(robot, X))
+        assert_score_parity(Kg.ravel(), Kr.ravel(), what=f"gram M={M} kind={kind}")
+
+
 def test_gram_equals_score_with_unit_alpha():
     """T2 cross-kernel identity: K[i, j] == fastron_score(x_j; supports X, alpha = e_i) bit for bit."""
     require_gpu()

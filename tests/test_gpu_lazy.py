@@ -66,3 +66,25 @@ def test_lazy_warm_start():
     torch.cuda.synchronize()
     assert fb.train_result(lazy["result"]) == fb.train_result(full["result"])
     assert np.array_equal(lazy["alpha"].cpu().numpy(), full["alpha"].cpu().numpy())
+
+
+@pytest.mark.parametrize("M", [3, 5])
+def test_lazy_odd_m_equals_full_gram(M):
+    """Odd M: the padded control point contributes exactly 0 to a computed column, as it
+    does in fastron_gram (same values, same trace)."""
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    wl = W.train_workload(700)
+    rng = np.random.default_rng(M)
+    robot = W.make_robot("m%d" % M, wl.robot.dh, rng.integers(1, 8, size=M), rng.uniform(-0.1, 0.1, size=(M, 3)))
+    y = W.capsule_aabb_labels(W.chain_points(oracle.fk(wl.robot, wl.X)), wl.cubes, wl.radius)
+    pos = fb.fastron_fk(robot, dev(wl.X))
+    K = fb.fastron_gram(pos, 0, wl.gamma)
+    assert np.all(np.diag(K.cpu().numpy()) == 1.0)
+    full = fb.fastron_train(K, dev(y), 1.0, 3000)
+    lazy = fb.fastron_train_lazy(pos, dev(y), 0, wl.gamma, 1.0, 3000, cache_cols=64)
+    torch.cuda.synchronize()
+    assert fb.train_result(full["result"]) == fb.train_result(lazy["result"])
+    assert np.array_equal(full["alpha"].cpu().numpy(), lazy["alpha"].cpu().numpy())
+    assert np.array_equal(full["F"].cpu().numpy(), lazy["F"].cpu().numpy())
