@@ -172,7 +172,7 @@ FkParams make_fk_params(const fastron_robot& r) {
     for (int m = 0; m < r.n_cp; ++m)
       if (r.cp_frame[m] == j) P.frame_list[n++] = m;
   }
-  for (int j = r.dof + 1; j <= FASTRON_MAX_DOF; ++j) P.frame_begin[j] = n;
+  for (int j = r.dof + 1; j <= FASTRON_MAX_DOF + 1; ++j) P.frame_begin[j] = n;  // ends of frames dof..16
   for (int m = 0; m < r.n_cp; ++m)
     for (int c = 0; c < 3; ++c) P.cp_off[m][c] = (double)r.cp_offset[m][c];
   return P;

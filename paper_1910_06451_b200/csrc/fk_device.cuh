@@ -29,7 +29,7 @@ struct FkParams {
   double sa[16];  // sin(alpha_i)
   double base_c[3][3];  // columns of the base rotation
   double base_p[3];
-  int32_t frame_begin[17];  // control points of frame j: frame_list[frame_begin[j] .. frame_begin[j+1])
+  int32_t frame_begin[18];  // control points of frame j (0..16): frame_list[frame_begin[j] .. frame_begin[j+1])
   int32_t frame_list[32];
   double cp_off[32][3];  // t_m, indexed by m
 };

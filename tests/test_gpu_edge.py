@@ -122,3 +122,13 @@ def test_cfg4_full_size_sampled():
             assert fall[e, idx[s_e]] > -1e-4
         else:
             assert idx[s_e] == -1
+
+
+def test_odd_m_robot_edges():
+    """Odd M (a padded control point) through the edge path: the FK prologue writes the
+    query side, which leaves the padded point at 0 (term exactly 0)."""
+    require_gpu()
+    wl = W.edge_workload(n_edges=200, n_supports=400)
+    rng = np.random.default_rng(5)
+    robot = W.make_robot("m5", wl.robot.dh, rng.integers(1, 8, size=5), rng.uniform(-0.1, 0.1, size=(5, 3)))
+    _check(robot, wl.qa, wl.qb, wl.n_interp, wl.supports, wl.alpha, 0, wl.gamma)

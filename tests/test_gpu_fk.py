@@ -72,3 +72,16 @@ def test_fk_planar_spec_examples():
     q = np.array([[0, 0], [np.pi / 2, 0], [np.pi / 2, np.pi / 2]], dtype=np.float32)
     got = positions_np(_fk(robot, q))
     np.testing.assert_allclose(got[:, 1], [[2, 0, 0], [0, 2, 0], [-1, 1, 0]], atol=3e-7)
+
+
+def test_fk_maximum_dof_and_control_points():
+    """D = 16 joints with random theta offsets, d, a and alpha (any real alpha, not only
+    0 / +-pi/2) and M = 32 control points on random frames with random offsets: the
+    largest robot the ABI accepts."""
+    require_gpu()
+    rng = np.random.default_rng(16)
+    dh = np.stack([rng.uniform(-1, 1, 16), rng.uniform(-0.2, 0.2, 16), rng.uniform(-0.2, 0.2, 16),
+                   rng.uniform(-np.pi, np.pi, 16)], axis=1)
+    robot = W.make_robot("d16m32", dh, rng.integers(0, 17, size=32), rng.uniform(-0.1, 0.1, size=(32, 3)))
+    q = rng.uniform(-np.pi, np.pi, size=(777, 16)).astype(np.float32)
+    _check(robot, q)
