@@ -184,3 +184,17 @@ def test_cfg5_gram_full_size_sampled_rows():
     for r, i in enumerate(rows):
         ref, _ = oracle.score(0, 5.0, opos, opos[i:i + 1], np.ones(1, np.float32))
         assert_score_parity(Kr[r], ref, what=f"cfg5 Gram row {i}")
+
+
+def test_train_cluster_path_trace_exact():
+    """n = 6,145 > one CTA's 6,144 register slots: Algorithm 1 runs on a 2-CTA cluster
+    (slices of 3,073 and 3,072, DSMEM candidate exchange); the trace, alpha and F must still
+    equal the oracle's on the same Gram."""
+    require_gpu()
+    robot, X = W.arm7(8), W.cfg5_gram_workload(6145)[1]
+    cubes = W.train_workload().cubes
+    y = W.capsule_aabb_labels(W.chain_points(oracle.fk(robot, X)), cubes, 0.05)
+    _, K = _gram(robot, X, 0, 5.0)
+    g = _gpu_train(K, y, 1.0, 20_000)
+    r = oracle.train(K.cpu().numpy().astype(np.float64), y, 1.0, 20_000)
+    _assert_same_run(g, r)
