@@ -53,7 +53,10 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t nb, int64_t& bi, 
 }
 
 #ifndef FASTRON_GRAM_RI4
-#define FASTRON_GRAM_RI4 1
+#define FASTRON_GRAM_RI4 1  // rows interleaved per pair loop at CPL = 4
+#endif
+#ifndef FASTRON_GRAM_RI2
+#define FASTRON_GRAM_RI2 kChunkRows  // ... at CPL <= 2
 #endif
 
 __host__ __device__ constexpr int gram_cpl(int mp) {  // columns per lane
@@ -69,7 +72,7 @@ __global__ void __launch_bounds__(kGT, gram_min_blocks(MP))
                 int64_t ldk) {
   constexpr int NP = MP / 2;
   constexpr int CPL = gram_cpl(MP);           // columns per lane
-  constexpr int RI = CPL >= 4 ? FASTRON_GRAM_RI4 : kChunkRows;  // rows interleaved per pair loop
+  constexpr int RI = CPL >= 4 ? FASTRON_GRAM_RI4 : FASTRON_GRAM_RI2;  // rows interleaved per pair loop
   constexpr int WC = 32 * CPL;                // columns per warp
   constexpr int G = kGB / WC;                 // column groups (warps sharing a row range)
   constexpr int R = kGW / G;                  // row groups
