@@ -1,0 +1,52 @@
+"""FastronModel (the host sequencing of the ABI calls, README usage): fit = Gram +
+Algorithm 1, query = FK + score, checked against the oracle on the same data."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from gpu_helpers import dev, require_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_fit_then_query_matches_oracle(kind):
+    require_gpu()
+    import torch
+    from paper_1910_06451_b200.model import FastronModel
+    tw = W.train_workload(1200)
+    y = W.capsule_aabb_labels(W.chain_points(oracle.fk(tw.robot, tw.X)), tw.cubes, tw.radius)
+    m = FastronModel(tw.robot, kind=kind, gamma=tw.gamma, iter_max=4000)
+    res = m.fit(dev(tw.X), dev(y))
+    assert res["n_support"] == len(m.supports) > 0
+    # the oracle's Algorithm 1 on the GPU Gram picks the same support set
+    pos = __import__("paper_1910_06451_b200").fastron_fk(tw.robot, dev(tw.X))
+    K = __import__("paper_1910_06451_b200").fastron_gram(pos, kind, tw.gamma).cpu().numpy().astype(np.float64)
+    r = oracle.train(K, y, 1.0, 4000)
+    assert np.array_equal(r["support"], np.flatnonzero(r["alpha"] != 0))
+    sup_X = m.supports.cpu().numpy()
+    assert np.array_equal(sup_X, tw.X[r["support"]])
+    # queries: scores against the model's support set and (fp32) weights
+    q = W.uniform_configs(np.random.default_rng(77), 20_000, 7)
+    s, l = m.query(dev(q))
+    torch.cuda.synchronize()
+    a32 = m.alpha.float().cpu().numpy()
+    qp, sp = oracle.fk(tw.robot, q), oracle.fk(tw.robot, sup_X)
+    f, _ = oracle.score(kind, tw.gamma, qp, sp, a32)
+    # R25: a trained alpha has large entries of both signs, so the fp32 rounding of each
+    # term scales with sum_i |alpha_i| k_i (the sum's condition), not with |f|
+    cond, _ = oracle.score(kind, tw.gamma, qp, sp, np.abs(a32))
+    err = np.abs(s.cpu().numpy().astype(np.float64) - f)
+    tol = np.maximum(np.maximum(1e-4 * np.abs(f), 1e-5), 1e-7 * cond)
+    assert np.all(err <= tol), (f"{np.sum(err > tol)} outside; max err/cond {np.max(err / cond):.2e}, "
+                                f"max |alpha| {np.abs(a32).max():.3g}")
+    lab = l.cpu().numpy()
+    sure = np.abs(f) > np.maximum(1e-4, 1e-7 * cond)
+    assert np.array_equal(lab[sure], np.where(f[sure] > 0, 1, -1))
+    print(f"kind={kind}: max err/cond {np.max(err / cond):.2e}, max |alpha| {np.abs(a32).max():.3g}")
+    # the training set is classified by its own margins' signs where they are certain
+    s_tr, _ = m.query(dev(tw.X))
+    F = r["F"]
+    sure = np.abs(F) > 1e-3
+    assert np.array_equal(np.sign(s_tr.cpu().numpy()[sure]), np.sign(F[sure]))
