@@ -711,7 +711,7 @@ fastron_status fastron_query(const fastron_robot* robot, const float* q, int64_t
       e = launch_fk(P, q + off * ldq, n, ldq, reinterpret_cast<float4*>(buf[0].pos), chunk, st);
       if (e == cudaSuccess)
         e = launch_score(reinterpret_cast<const float4*>(buf[0].pos), n, chunk, packed, ns, M, k.kind, c,
-                         score ? score + off : nullptr, label ? label + off : nullptr, partial, st);
+                         score ? score + off : nullptr, label ? label + off : nullptr, partial, st, nullptr, nq);
       if (e != cudaSuccess) return cuda_status(e, "fastron_query");
     }
     return FASTRON_OK;
@@ -753,7 +753,7 @@ fastron_status fastron_query(const fastron_robot* robot, const float* q, int64_t
     if (e == cudaSuccess) e = launch_fk(P, qdev, n, ldq_dev, reinterpret_cast<float4*>(buf[b].pos), chunk, cs[b]);
     if (e == cudaSuccess)
       e = launch_score(reinterpret_cast<const float4*>(buf[b].pos), n, chunk, packed, ns, M, k.kind, c, sdev, ldev,
-                       partials[b], cs[b]);
+                       partials[b], cs[b], nullptr, nq);
     cudaEventRecord(ev_used[b], cs[b]);
     // results out
     cudaStreamWaitEvent(d2h, ev_used[b], 0);

@@ -51,7 +51,7 @@ size_t score_partial_bytes(int64_t nq, int64_t ns, int M);
 
 cudaError_t launch_score(const float4* qpos, int64_t nq, int64_t ldq, const float* packed, int64_t ns, int M, int kind,
                          float scale, float* score, int8_t* label, double* partial, cudaStream_t st,
-                         double* score64 = nullptr);
+                         double* score64 = nullptr, int64_t plan_nq = 0);
 
 // K4: one round of the fused edge check (interpolate -> FK -> score -> warp vote).
 struct EdgeRound {

@@ -115,6 +115,7 @@ struct ScoreArgs {
   int32_t* hit_index;
   double denom;  // M for the FK kernel's 1/M mean (Eq. 4), 1 for the joint-space kernel
   double* score64;  // optional fp64 scores (margins for a warm start)
+  int64_t plan_nq;  // host only: batch size the split count is planned for (0: nq)
 };
 
 // Position k of the visiting order of round r, lane l: evens first, then odds (R11).
@@ -381,15 +382,31 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ S
 // ---------------------------------------------------------------------------------
 // planning + dispatch
 // ---------------------------------------------------------------------------------
+// Support splits. Measured on the headline (tools/split_probe.sh): the time falls as the
+// per-CTA work shrinks — 2 splits 41.7 ms, 4: 40.9, 8: 40.9, 16: 40.8 — because the
+// last partial wave costs about one CTA's work, and the hardware block scheduler balances
+// many short CTAs well. The plan therefore aims at ~kTargetWaves waves of CTAs, bounded
+// by the tile count and by the fp64 partial buffer (s * nq doubles <= kPartialBudget).
+constexpr int64_t kTargetWaves = 32;
+constexpr int64_t kPartialBudget = (int64_t)1 << 23;  // doubles (64 MB)
+
+static int64_t split_env() {
+  const char* e = getenv("FASTRON_SCORE_SPLITS");  // experiments: force a split count
+  return e ? atoll(e) : 0;
+}
+
 int score_max_splits(int64_t nq, int64_t ns, int M) {
   const int64_t qblocks = (nq + score_queries_per_cta(M) - 1) / score_queries_per_cta(M);
   const int64_t tiles = n_support_tiles(ns);
   if (qblocks <= 0 || tiles <= 1) return 1;
-  // enough units for ~8 waves of 148 SMs x 4 CTAs; never more splits than tiles
-  int64_t cap = (8 * 148 * 4 + qblocks - 1) / qblocks;
-  cap = cap < 1 ? 1 : cap;
-  cap = cap > 64 ? 64 : cap;
-  return (int)(cap < tiles ? cap : tiles);
+  const int64_t slots_max = (int64_t)device_info().sms * 4;  // >= any resident-CTA count of K2
+  int64_t cap = (kTargetWaves * slots_max + qblocks - 1) / qblocks;
+  const int64_t budget = kPartialBudget / (nq > 0 ? nq : 1);
+  if (cap > budget) cap = budget;
+  const int64_t forced = split_env();
+  if (forced > cap) cap = forced;
+  if (cap > tiles) cap = tiles;
+  return (int)(cap < 1 ? 1 : cap);
 }
 
 size_t score_partial_bytes(int64_t nq, int64_t ns, int M) {
@@ -420,17 +437,17 @@ static ScorePlan make_plan(int64_t nq, int64_t ns, int M, int ctas_per_sm) {
   p.n_tiles = n_support_tiles(ns);
   const int64_t slots = (int64_t)device_info().sms * ctas_per_sm;
   const int max_s = score_max_splits(nq, ns, M);
-  int best = 1;
-  double best_score = -1.0;
-  for (int s = 1; s <= max_s; ++s) {
+  // the smallest split count reaching ~kTargetWaves waves (capped by max_s), moved to a
+  // count whose splits are all non-empty
+  int64_t want = p.n_qblocks > 0 ? (kTargetWaves * slots + p.n_qblocks - 1) / p.n_qblocks : 1;
+  if (const int64_t forced = split_env()) want = forced;
+  if (want > max_s) want = max_s;
+  if (want < 1) want = 1;
+  int best = (int)want;
+  for (int s = (int)want; s >= 1; --s) {
     const int64_t tps = (p.n_tiles + s - 1) / s;
-    const int64_t s_eff = tps > 0 ? (p.n_tiles + tps - 1) / tps : 1;  // splits actually non-empty
-    if (s_eff != s) continue;
-    const int64_t units = p.n_qblocks * s;
-    const int64_t waves = (units + slots - 1) / slots;
-    const double eff = (double)units / (double)(waves * slots);
-    const double sc = eff - 0.004 * s;  // mild preference for fewer splits (partials + finalize)
-    if (sc > best_score + 1e-12) { best_score = sc; best = s; }
+    const int64_t s_eff = tps > 0 ? (p.n_tiles + tps - 1) / tps : 1;
+    if (s_eff == s) { best = s; break; }
   }
   p.n_splits = best;
   p.tiles_per_split = (int32_t)(p.n_tiles > 0 ? (p.n_tiles + best - 1) / best : 0);
@@ -439,7 +456,11 @@ static ScorePlan make_plan(int64_t nq, int64_t ns, int M, int ctas_per_sm) {
 
 template <int MP, int KIND, int MODE>
 static cudaError_t run_score(const ScoreArgs& base, const FkParams& P, int64_t nq, int64_t ns, cudaStream_t st) {
-  const ScorePlan plan = make_plan(nq, ns, base.M, score_ctas_per_sm<MP, KIND, MODE>());
+  // the split count (and so the fp64 summation order) follows the whole batch: a chunk of
+  // a larger batch is planned like the batch, so chunked and single-launch scores agree
+  // bit for bit
+  ScorePlan plan = make_plan(base.plan_nq > nq ? base.plan_nq : nq, ns, base.M, score_ctas_per_sm<MP, KIND, MODE>());
+  plan.n_qblocks = (nq + score_queries_per_cta(base.M) - 1) / score_queries_per_cta(base.M);
   ScoreArgs A = base;
   A.n_tiles = plan.n_tiles;
   A.n_splits = plan.n_splits;
@@ -542,9 +563,10 @@ cudaError_t launch_score_joint(const float4* qpts, int64_t nq, const float* pack
 
 cudaError_t launch_score(const float4* qpos, int64_t nq, int64_t ldq, const float* packed, int64_t ns, int M, int kind,
                          float scale, float* score, int8_t* label, double* partial, cudaStream_t st,
-                         double* score64) {
+                         double* score64, int64_t plan_nq) {
   if (nq <= 0) return cudaSuccess;
   ScoreArgs A = {};
+  A.plan_nq = plan_nq;
   A.score64 = score64;
   A.qpos = qpos;
   A.ldq = ldq;
