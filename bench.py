@@ -355,6 +355,23 @@ def _time_rows(fb, torch, kind):
     res_t1["fk_speedup_vs_rbf"] = res_t1["rbf_joint"]["ms"] / res_t1["fk"]["ms"]
     res_t1["paper_query_us"] = {"fk": 2.5, "rbf": 4.6, "note": "PAPER.md:290-291, single queries, unstated CPU"}
     rows["table1_query_sizes"] = res_t1
+    # small batches (a planner asking a few configurations at a time): per-call latency of
+    # FK + score for nq queries, stream launches vs a captured CUDA graph, at the Table I
+    # FK model size (|S| = 303) and the headline model (|S| = 20,000)
+    lat = {}
+    for ns in (303, 20_000):
+        sp = fb.fastron_fk(hw.robot, torch.from_numpy(hw.supports[:ns]).cuda())
+        mdl = fb.fastron_model_pack(sp, torch.from_numpy(hw.alpha[:ns]).cuda(), kind, hw.gamma)
+        for nq in (1, 64, 4096):
+            qs = qd[:nq].contiguous()
+            qp = torch.empty((8, nq, 4), device="cuda")
+            sc = torch.empty(nq, device="cuda")
+            lb = torch.empty(nq, dtype=torch.int8, device="cuda")
+            wsl = torch.empty(max(256, fb.load_library().fastron_score_packed_workspace_bytes(nq, ns, 8)),
+                              dtype=torch.uint8, device="cuda")
+            fn = lambda: (fb.fastron_fk(hw.robot, qs, pos=qp), fb.fastron_score_packed(qp, mdl, sc, lb, workspace=wsl))
+            lat[f"S{ns}_q{nq}"] = {"stream_us": timed(fn, 200) * 1e3, "graph_us": graphed(fn, 200) * 1e3}
+    rows["small_batch_latency"] = lat
     # cfg4: 10k edges x 64 points, 3k supports, early exit
     ew = W.edge_workload()
     spos = fb.fastron_fk(ew.robot, torch.from_numpy(ew.supports).cuda())
