@@ -185,6 +185,8 @@ __global__ void __launch_bounds__(256) edge_fk_kernel(const __grid_constant__ Sc
 }
 
 template <int MP, int KIND, int MODE>
+// (no min-blocks argument: with one, ptxas allocates 182+ registers and only 2 CTAs fit
+// per SM — 4 % slower; without, 158 registers and 3 CTAs)
 __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ ScoreArgs A,
                                                     const __grid_constant__ FkParams P) {
   constexpr int QT = qt_for(MP);
