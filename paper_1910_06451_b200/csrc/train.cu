@@ -62,6 +62,11 @@ struct Cand {     // a (key, index) winner with its payload
   int32_t pad;
 };
 
+struct __align__(16) CandBox {  // an inbox entry: 16-byte aligned for the vector DSMEM stores
+  Cand c;
+  int32_t pad2[2];
+};
+
 struct Decision {
   int32_t action;
   int32_t idx;    // row of the rank-one update = slot whose Y changes
@@ -168,6 +173,38 @@ __device__ __forceinline__ int warp_arglane(uint64_t key, int idx) {
   return own ? __ffs(own) - 1 : -1;
 }
 
+// ---- cluster exchange of the CTA winners (C > 1) ----
+// CTA r's winner goes into slot [b][r] of every CTA's inbox by st.async (DSMEM stores that
+// complete transaction bytes on the receiver's mbarrier); each CTA then waits on its own
+// inbox barrier — a point-to-point hand-off instead of a cluster-wide barrier.
+constexpr uint32_t kCandMsgBytes = 40;  // key, G | Y, idx, y | slot, pad
+
+__device__ __forceinline__ uint32_t cluster_addr(const void* p, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_v2b64(uint32_t dst, uint64_t a, uint64_t b, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];"
+               ::"r"(dst), "l"(a), "l"(b), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void st_async_v2b32(uint32_t dst, uint32_t a, uint32_t b, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];"
+               ::"r"(dst), "r"(a), "r"(b), "r"(bar) : "memory");
+}
+// wait with cluster-scope acquire: the peers' st.async data is visible afterwards
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
 __device__ __forceinline__ float ld_evict_last(const float* p, uint64_t pol) {
   float v;
   asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
@@ -242,7 +279,8 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
   float* s_rec = reinterpret_cast<float*>(smem_raw + ((A.chunk * 8 + 15) & ~15ll));
   int32_t* s_slot = reinterpret_cast<int32_t*>(s_rec + (LAZY ? A.chunk * LNP * 8 : 0));
   __shared__ Cand s_warp[2][kTrainWarps];
-  __shared__ Cand s_cta[2];
+  __shared__ CandBox s_inbox[2][kMaxCluster];               // C > 1: the CTA winners of an exchange
+  __shared__ __align__(8) uint64_t s_inbar[2];              // their arrival barriers
   __shared__ int32_t s_cta_cnt[2];
   __shared__ int32_t s_cnt[kTrainWarps];
 
@@ -277,7 +315,13 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
       for (int w = 0; w < LNP * 2; ++w) dst[w] = src[w];
     }
   }
-  // initial count(alpha != 0) over the cluster
+  if (tid == 0) {  // inbox barriers: one local arrival (with the expected bytes) per exchange
+    mbar_init(&s_inbar[0], 1);
+    mbar_init(&s_inbar[1], 1);
+    fence_barrier_init();
+  }
+  // initial count(alpha != 0) over the cluster (its cluster barrier also publishes the
+  // initialised inbox barriers to the peers)
   {
     const int wsum = (int)__reduce_add_sync(0xffffffffu, (unsigned)cnt0);
     if (lane == 0) s_cnt[warp] = wsum;
@@ -291,6 +335,30 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
   }
   int64_t nnz = 0;
   for (int r = 0; r < C; ++r) nnz += *cluster.map_shared_rank(&s_cta_cnt[0], r);
+
+  // C > 1: exchange number ex uses inbox slot ex & 1 at barrier phase (ex >> 1) & 1. A peer
+  // cannot send into a slot again before this CTA has consumed it: its next message there
+  // needs this CTA's message of the exchange in between, sent only after this CTA's
+  // barrier that follows its reads.
+  uint32_t ex = 0;
+  auto cluster_best = [&](const Cand& mine, bool for_max) -> Cand {  // mine: warp 0's CTA winner
+    const int b = (int)(ex & 1u);
+    if (warp == 0) {
+      if (lane == 0) mbar_expect_tx(&s_inbar[b], (uint32_t)C * kCandMsgBytes);
+      if (lane < C) {  // lane r delivers this CTA's winner to rank r
+        const uint32_t dst = cluster_addr(&s_inbox[b][rank], lane);
+        const uint32_t bar = cluster_addr(&s_inbar[b], lane);
+        st_async_v2b64(dst, mine.key, (uint64_t)__double_as_longlong(mine.G), bar);
+        st_async_v2b64(dst + 16, (uint64_t)__double_as_longlong(mine.Y),
+                       ((uint64_t)(uint32_t)mine.y << 32) | (uint32_t)mine.idx, bar);
+        st_async_v2b32(dst + 32, (uint32_t)mine.slot, 0u, bar);
+      }
+    }
+    mbar_wait_cluster(&s_inbar[b], (ex >> 1) & 1u);
+    ++ex;
+    return for_max ? warp_best<true>(lane < C ? s_inbox[b][lane].c : cand_none(true))
+                   : warp_best<false>(lane < C ? s_inbox[b][lane].c : cand_none(false));
+  };
 
   // loop invariants: clamped K-row offsets of the slots and the label sign bit of each
   // slot as an fp64 high-word mask (y_j fl(d K) is fl(d K) with its sign flipped)
@@ -415,12 +483,9 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
       const Cand best = warp_best<false>(lane < kTrainWarps ? s_warp[parity][lane] : cand_none(false));
       d = decide_min(best, iters, nnz, nfree, A);
     } else {
-      if (warp == 0) {
-        const Cand best = warp_best<false>(lane < kTrainWarps ? s_warp[parity][lane] : cand_none(false));
-        if (lane == 0) s_cta[parity] = best;
-      }
-      cluster.sync();
-      const Cand best = warp_best<false>(lane < C ? *cluster.map_shared_rank(&s_cta[parity], lane) : cand_none(false));
+      Cand mine = cand_none(false);
+      if (warp == 0) mine = warp_best<false>(lane < kTrainWarps ? s_warp[parity][lane] : cand_none(false));
+      const Cand best = cluster_best(mine, false);
       d = decide_min(best, iters, nnz, nfree, A);
     }
     PROF_MARK(3);
@@ -456,12 +521,9 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
         const Cand best = warp_best<true>(lane < kTrainWarps ? s_warp[q][lane] : cand_none(true));
         d = decide_removal(d, best, nfree, A);
       } else {
-        if (warp == 0) {
-          const Cand best = warp_best<true>(lane < kTrainWarps ? s_warp[q][lane] : cand_none(true));
-          if (lane == 0) s_cta[q] = best;
-        }
-        cluster.sync();
-        const Cand best = warp_best<true>(lane < C ? *cluster.map_shared_rank(&s_cta[q], lane) : cand_none(true));
+        Cand mine = cand_none(true);
+        if (warp == 0) mine = warp_best<true>(lane < kTrainWarps ? s_warp[q][lane] : cand_none(true));
+        const Cand best = cluster_best(mine, true);
         d = decide_removal(d, best, nfree, A);
       }
       parity = q;  // buffers of parity q were used last; the loop flips back below
