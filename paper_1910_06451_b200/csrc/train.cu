@@ -16,9 +16,11 @@
 //   2. apply the pending rank-one update G_j += y_j fl(delta K_ij) (Eq. 8) and track the
 //      thread's min of G (two interleaved chains; lowest index on ties, R9);
 //   3. warp REDUX on order-preserving integer keys -> the owning lane writes the warp
-//      candidate with Y and y of the winner -> __syncthreads -> warp 0 reduces the warp
-//      candidates (with C > 1: CTA candidates exchanged through DSMEM behind one
-//      cluster barrier) and takes the decision of Alg. 1 -> __syncthreads.
+//      candidate with Y and y of the winner -> __syncthreads -> every warp reduces the
+//      warp candidates and takes the (identical) decision of Alg. 1 itself, so no second
+//      barrier is needed. With C > 1, warp 0 first sends the CTA winner into every CTA's
+//      inbox (st.async into DSMEM, completing bytes on the receiver's mbarrier) and all
+//      warps wait on their own inbox barrier before reducing the C CTA winners.
 // The redundant-support scan argmax_{alpha != 0} y (F - alpha) is only
 // needed when the add branch does not `continue` (min margin > 0, or the S_max gate
 // blocks the add); it runs as a second pass in exactly those iterations.
