@@ -207,9 +207,15 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase)
       : "memory");
 }
 
+// K rows are read-only for the kernel's lifetime: the non-coherent path. The lazy column
+// cache is written by this kernel, so its reads take the coherent path.
+template <bool COHERENT>
 __device__ __forceinline__ float ld_evict_last(const float* p, uint64_t pol) {
   float v;
-  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  if (COHERENT)
+    asm volatile("ld.global.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  else
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
   return v;
 }
 
@@ -276,10 +282,13 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* s_Y = reinterpret_cast<double*>(smem_raw);  // [chunk], owner-thread access only
-  // lazy mode: the slice's pre-scaled points (records of the scoring tile layout) and the
-  // cache slot of each local index's K column (owner-thread access only)
-  float* s_rec = reinterpret_cast<float*>(smem_raw + ((A.chunk * 8 + 15) & ~15ll));
-  int32_t* s_slot = reinterpret_cast<int32_t*>(s_rec + (LAZY ? A.chunk * LNP * 8 : 0));
+  // lazy mode: the slice's pre-scaled points as structure-of-arrays f32x2 planes
+  // s_pts[(p * 3 + coord) * chunk + j] (control points 2p, 2p+1 of point j): a thread reads
+  // its own points, so consecutive lanes read consecutive 8-byte words — conflict-free
+  // (a per-point record layout put every lane on the same banks: 32-way conflicts, ~11k
+  // cycles per computed column). Then the cache slot of each local index's K column.
+  f2* s_pts = reinterpret_cast<f2*>(smem_raw + ((A.chunk * 8 + 15) & ~15ll));
+  int32_t* s_slot = reinterpret_cast<int32_t*>(s_pts + (LAZY ? A.chunk * LNP * 3 : 0));
   __shared__ Cand s_warp[2][kTrainWarps];
   __shared__ CandBox s_inbox[2][kMaxCluster];               // C > 1: the CTA winners of an exchange
   __shared__ __align__(8) uint64_t s_inbar[2];              // their arrival barriers
@@ -312,9 +321,14 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
     if (LAZY && live) {
       s_slot[j] = -1;
       const int64_t g = lo + j;
-      const float4* src = reinterpret_cast<const float4*>(A.packed + (g / kTileSupports) * LTF + (g % kTileSupports) * LNP * 8);
-      float4* dst = reinterpret_cast<float4*>(s_rec + (int64_t)j * LNP * 8);
-      for (int w = 0; w < LNP * 2; ++w) dst[w] = src[w];
+      const float* src = A.packed + (g / kTileSupports) * LTF + (g % kTileSupports) * LNP * 8;
+      for (int p = 0; p < LNP; ++p) {
+        const float4 xy = *reinterpret_cast<const float4*>(src + p * 8);
+        const float2 zz = *reinterpret_cast<const float2*>(src + p * 8 + 4);
+        s_pts[(int64_t)(p * 3 + 0) * A.chunk + j] = pk(xy.x, xy.y);
+        s_pts[(int64_t)(p * 3 + 1) * A.chunk + j] = pk(xy.z, xy.w);
+        s_pts[(int64_t)(p * 3 + 2) * A.chunk + j] = pk(zz.x, zz.y);
+      }
     }
   }
   if (tid == 0) {  // inbox barriers: one local arrival (with the expected bytes) per exchange
@@ -382,6 +396,7 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
 
 #ifdef FASTRON_TRAIN_PROF
   unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long prof_miss = 0, n_miss = 0;  // lazy mode: cycles in computed columns
   unsigned long long tp = clock64();
 #define PROF_MARK(i)                         \
   do {                                       \
@@ -402,8 +417,11 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
       if (!LAZY || upd_slot >= 0) {
         const float* Krow = LAZY ? A.cache + (int64_t)upd_slot * A.n + lo : A.K + (int64_t)upd_i * A.ldk + lo;
 #pragma unroll
-        for (int k = 0; k < EPT; ++k) kr[k] = ld_evict_last(Krow + koff[k], pol);
+        for (int k = 0; k < EPT; ++k) kr[k] = ld_evict_last<LAZY>(Krow + koff[k], pol);
       } else if (LAZY) {
+#ifdef FASTRON_TRAIN_PROF
+        const unsigned long long t_miss = clock64();
+#endif
         // computeKernelMatrixColumn(i): K(X_j, X_i) for the thread's slots,
         // with the same term function and summation order as fastron_gram (bit-identical)
         const float* wr = A.packed + (int64_t)(upd_i / kTileSupports) * LTF + (upd_i % kTileSupports) * LNP * 8;
@@ -423,13 +441,13 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
         }
 #pragma unroll
         for (int k = 0; k < EPT; ++k) {
-          const float* rec = s_rec + (int64_t)koff[k] * LNP * 8;
           f2 acc;
 #pragma unroll
           for (int p = 0; p < LNP; ++p) {
-            const float4 xy = *reinterpret_cast<const float4*>(rec + p * 8);
-            const float2 zz = *reinterpret_cast<const float2*>(rec + p * 8 + 4);
-            const f2 t = term_pair<LKIND>(pk(xy.x, xy.y), pk(xy.z, xy.w), pk(zz.x, zz.y), vx[p], vy[p], vz[p]);
+            const f2 ux = s_pts[(int64_t)(p * 3 + 0) * A.chunk + koff[k]];
+            const f2 uy = s_pts[(int64_t)(p * 3 + 1) * A.chunk + koff[k]];
+            const f2 uz = s_pts[(int64_t)(p * 3 + 2) * A.chunk + koff[k]];
+            const f2 t = term_pair<LKIND>(ux, uy, uz, vx[p], vy[p], vz[p]);
             acc = p == 0 ? t : add2(acc, t);
           }
           const float ks = pair_sum(acc);
@@ -438,6 +456,17 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
           const int j = k * kTrainNT + tid;
           if (upd_new_slot >= 0 && j < len) A.cache[(int64_t)upd_new_slot * A.n + lo + j] = v;
         }
+#ifdef FASTRON_TRAIN_PROF
+        {
+          // force completion of the computed values before reading the clock
+          float sink = 0.f;
+#pragma unroll
+          for (int k = 0; k < EPT; ++k) sink += kr[k];
+          if (sink == -1.f) prof_miss += 1;
+          prof_miss += clock64() - t_miss;
+          ++n_miss;
+        }
+#endif
       }
     }
     double m0 = INFINITY, m1 = INFINITY;  // two interleaved chains (even / odd k)
@@ -558,6 +587,7 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
   }
 
 #ifdef FASTRON_TRAIN_PROF
+  if (tid == 0 && rank == 0 && n_miss) printf("train prof computed columns %llu, %.0f cycles each\n", n_miss, (double)prof_miss / n_miss);
   if (tid == 0 && rank == 0)
     printf("train prof cycles/iter: scan %.0f merge+key %.0f argbest %.0f payload %.0f bar %.0f decide %.0f - %.0f tail %.0f (iters %lld)\n",
            (double)prof[0] / iters, (double)prof[6] / iters, (double)prof[7] / iters, (double)prof[1] / iters,
@@ -697,7 +727,7 @@ cudaError_t launch_train(const float* K, int64_t n, int64_t ldk, const int8_t* y
 // ---- lazy-column mode ----
 constexpr int64_t kLazySmem = 200 * 1024;  // shared-memory budget per CTA
 
-static int64_t lazy_bytes_per_slot(int MP) { return 8 + 4 + (int64_t)(MP / 2) * 32; }
+static int64_t lazy_bytes_per_slot(int MP) { return 8 + 4 + (int64_t)(MP / 2) * 24; }
 
 int64_t train_lazy_max_n(int M) {
   const int MP = padded_m(M);
@@ -747,7 +777,7 @@ cudaError_t launch_train_lazy(const float* packed, int64_t n, int M, int kind, c
   A.M = M;
   A.m_pow2 = (M & (M - 1)) == 0;
   A.inv_m = 1.0f / (float)M;
-  const size_t smem = (size_t)((A.chunk * 8 + 15) & ~15ll) + (size_t)A.chunk * (MP / 2) * 32 + (size_t)A.chunk * 4;
+  const size_t smem = (size_t)((A.chunk * 8 + 15) & ~15ll) + (size_t)A.chunk * (MP / 2) * 24 + (size_t)A.chunk * 4;
   cudaError_t e;
   switch (MP) {
 #define FASTRON_LCASE(mp)                                                                              \
