@@ -189,3 +189,22 @@ def test_cfg5_full_size_sampled():
     idx = np.unique(np.concatenate([rng.choice(len(s), 1000, replace=False), np.argsort(np.abs(s))[:500]]))
     f, _ = _ref_scores(wl.robot, wl.supports, wl.alpha, wl.queries[idx], 0, wl.gamma)
     assert_score_parity(s[idx], f, l[idx], what="cfg5 full-size sample")
+
+
+def test_query_chunks_planned_like_the_batch():
+    """fastron_query streams 256k-query chunks; each chunk is planned like the whole batch
+    (same support splits, so the same fp64 summation order), so the chunked scores equal
+    a single launch over the batch bit for bit — at the headline model size, where the
+    split count depends on the batch size."""
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    wl = W.score_workload("headline", n_queries=600_000)
+    spos = fb.fastron_fk(wl.robot, dev(wl.supports))
+    alpha = dev(wl.alpha)
+    s_dev, l_dev = _gpu_scores(wl.robot, wl.supports, wl.alpha, wl.queries, 0, wl.gamma)
+    qh = torch.from_numpy(wl.queries).pin_memory()
+    sh = torch.empty(len(wl.queries), dtype=torch.float32).pin_memory()
+    lh = torch.empty(len(wl.queries), dtype=torch.int8).pin_memory()
+    fb.fastron_query(wl.robot, qh, spos, alpha, 0, wl.gamma, score=sh, label=lh)
+    assert np.array_equal(sh.numpy(), s_dev) and np.array_equal(lh.numpy(), l_dev)
