@@ -459,6 +459,7 @@ def run_ours(args):
     ms_total = t0.elapsed_time(t1)
     fk_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
     sc_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
+    step_each = np.array([e[0].elapsed_time(e[2]) for e in ev])  # per-step FK start -> score end
     ms_step = fd.max_over_ranks(ms_total / args.steps, device="cuda")
     value = fd.aggregate_rate(Q, ws, ms_step)
     clocks = clk.summary()
@@ -526,6 +527,8 @@ def run_ours(args):
                            "parallelism": f"dp{ws} (query shards, replicated model)",
                            "l2": "inputs larger than L2 (28 MB queries + 128 MB positions per step > 126 MB)"},
                 "kernel_evals_per_s": value * S,
+                "step_ms": {"min": float(step_each.min()), "median": float(np.median(step_each)),
+                            "max": float(step_each.max())},
                 "roofline": roof,
                 "cpu_baseline": base,
                 "e2e": {"value": fd.aggregate_rate(Q, ws, e2e_ms), "unit": UNIT, "h2d_bytes_per_step": Q * wl.robot.dof * 4,
