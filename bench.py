@@ -108,6 +108,16 @@ def _dist():
     return fd.world()
 
 
+def _cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(wl, target_s=12.0):
     """The oracle as it stands, on this host's cores, on a bounded sample of the workload:
     the first Qs queries of the batch against all supports (FK + fp64 score)."""
@@ -131,7 +141,8 @@ def cpu_baseline(wl, target_s=12.0):
         dt1 = run(n1)
     finally:
         oracle.set_num_threads(cores)
-    return {"value": nq / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+    return {"value": nq / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": _cpu_model(),
+            "host_cpus": os.cpu_count(),
             "sample": f"first {nq} of the {len(wl.queries)} headline queries x all {len(wl.supports)} supports "
                       f"(fp64 FK + score, OpenMP), {dt:.1f} s",
             "kernel_evals_per_s": nq * len(wl.supports) / dt,
@@ -165,6 +176,7 @@ def run_reference(args):
                        "n_cp": wl.robot.n_cp, "dof": wl.robot.dof, "gamma": wl.gamma,
                        "kernel": "gaussian" if wl.kind == 0 else "rq"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                             "cpu_model": _cpu_model(),
                              "sample": f"{nq} queries x {len(wl.supports)} supports per step"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
