@@ -2,7 +2,7 @@
 headline size, against the fp64 oracle, splitting the error by source (R24).
 Test infrastructure: it reads only oracle/ and workloads/."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import oracle, workloads as W
 

@@ -1,7 +1,7 @@
 """Time the headline step and measure score error stats for one library build
 (FASTRON_LIB env selects the .so). Prints one JSON line."""
 import json, os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import paper_1910_06451_b200 as fb, workloads as W, oracle
 wl = W.score_workload("headline", kind=int(os.environ.get("KIND", "0")))
