@@ -13,6 +13,8 @@
 #include <mutex>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges are free unless a profiler attaches
+
 #include "../../include/fastron.h"
 #include "fastron_device.cuh"
 #include "internal.h"
@@ -70,6 +72,12 @@ fastron_status cuda_status(cudaError_t e, const char* where) {
   } while (0)
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// One NVTX range per ABI call (host-side enqueue span), named after the entry point.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 // ---- optional content validation (fastron_set_validation, FASTRON_VALIDATE=1) ----
 std::atomic<int> g_validate{-1};
@@ -221,6 +229,7 @@ int32_t fastron_validation(void) { return validation_on() ? 1 : 0; }
 
 fastron_status fastron_fk(const fastron_robot* robot, const float* q, int64_t n, int64_t ldq, float* pos, int64_t ldpos,
                           void* stream) {
+  NvtxRange nvtx_range_("fastron_fk");
   fastron_status s = check_robot(robot);
   if (s != FASTRON_OK) return s;
   FASTRON_REQUIRE(n >= 0, "n must be >= 0");
@@ -242,6 +251,7 @@ size_t fastron_score_workspace_bytes(int64_t nq, int64_t ns, int32_t n_cp) {
 fastron_status fastron_score(const float* qpos, int64_t nq, int64_t ldq, const float* spos, const float* alpha,
                              int64_t ns, int64_t lds, int32_t n_cp, fastron_kernel k, float* score, int8_t* label,
                              void* workspace, size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_range_("fastron_score");
   fastron_status s = check_kernel(k);
   if (s != FASTRON_OK) return s;
   FASTRON_REQUIRE(nq >= 0 && ns >= 0, "nq and ns must be >= 0");
@@ -281,6 +291,7 @@ size_t fastron_model_bytes(int64_t ns, int32_t n_cp) {
 
 fastron_status fastron_model_pack(const float* spos, const float* alpha, int64_t ns, int64_t lds, int32_t n_cp,
                                   fastron_kernel k, void* packed, size_t packed_bytes_given, void* stream) {
+  NvtxRange nvtx_range_("fastron_model_pack");
   fastron_status s = check_kernel(k);
   if (s != FASTRON_OK) return s;
   FASTRON_REQUIRE(ns >= 0, "ns must be >= 0");
@@ -307,6 +318,7 @@ size_t fastron_score_packed_workspace_bytes(int64_t nq, int64_t ns, int32_t n_cp
 fastron_status fastron_score_packed(const float* qpos, int64_t nq, int64_t ldq, const void* packed, int64_t ns,
                                     int32_t n_cp, fastron_kernel k, float* score, int8_t* label, void* workspace,
                                     size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_range_("fastron_score_packed");
   fastron_status s = check_kernel(k);
   if (s != FASTRON_OK) return s;
   FASTRON_REQUIRE(nq >= 0 && ns >= 0, "nq and ns must be >= 0");
@@ -330,6 +342,7 @@ fastron_status fastron_score_packed(const float* qpos, int64_t nq, int64_t ldq, 
 fastron_status fastron_score_packed_f64(const float* qpos, int64_t nq, int64_t ldq, const void* packed, int64_t ns,
                                         int32_t n_cp, fastron_kernel k, double* score64, void* workspace,
                                         size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_range_("fastron_score_packed_f64");
   fastron_status s = check_kernel(k);
   if (s != FASTRON_OK) return s;
   FASTRON_REQUIRE(nq >= 0 && ns >= 0, "nq and ns must be >= 0");
@@ -357,6 +370,7 @@ size_t fastron_gram_workspace_bytes(int64_t n, int32_t n_cp) {
 
 fastron_status fastron_gram(const float* pos, int64_t n, int64_t ldp, int32_t n_cp, fastron_kernel k, float* K,
                             int64_t ldk, void* workspace, size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_range_("fastron_gram");
   fastron_status s = check_kernel(k);
   if (s != FASTRON_OK) return s;
   FASTRON_REQUIRE(n >= 0, "n must be >= 0");
@@ -381,6 +395,7 @@ int64_t fastron_train_max_n(void) { return train_max_n(); }
 fastron_status fastron_train(const float* K, int64_t n, int64_t ldk, const int8_t* y, double beta, int64_t iter_max,
                              int64_t s_max, double* alpha_inout, double* F_inout, int32_t* support_idx, int32_t* trace,
                              fastron_train_result* result, void* stream) {
+  NvtxRange nvtx_range_("fastron_train");
   FASTRON_REQUIRE(n >= 0 && iter_max >= 0 && s_max >= 0, "n, iter_max and s_max must be >= 0");
   FASTRON_REQUIRE(std::isfinite(beta) && beta >= 1.0, "beta must be >= 1 (PAPER.md:189), got %g", beta);
   FASTRON_REQUIRE(result != nullptr, "result is NULL");
@@ -415,6 +430,7 @@ fastron_status fastron_train_lazy(const float* pos, int64_t n, int64_t ldp, int3
                                   double* alpha_inout, double* F_inout, int32_t* support_idx, int32_t* trace,
                                   fastron_train_result* result, int64_t cache_cols, void* workspace,
                                   size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_range_("fastron_train_lazy");
   fastron_status s = check_kernel(k);
   if (s != FASTRON_OK) return s;
   FASTRON_REQUIRE(n >= 0 && iter_max >= 0 && s_max >= 0 && cache_cols >= 0, "sizes must be >= 0");
@@ -451,6 +467,7 @@ fastron_status fastron_train_lazy(const float* pos, int64_t n, int64_t ldp, int3
 fastron_status fastron_active_samples(const float* sup, int64_t ns, int64_t lds, int32_t dof, int32_t n_near,
                                       const float* z, const float* sigma, const float* u, int64_t n_uniform,
                                       const float* lo, const float* hi, float* out, int64_t ldo, void* stream) {
+  NvtxRange nvtx_range_("fastron_active_samples");
   FASTRON_REQUIRE(ns >= 0 && n_near >= 0 && n_uniform >= 0, "sizes must be >= 0");
   FASTRON_REQUIRE(dof >= 1 && dof <= FASTRON_MAX_DOF, "dof must be in [1,16], got %d", dof);
   if (ns * n_near + n_uniform == 0) return FASTRON_OK;
@@ -463,6 +480,7 @@ fastron_status fastron_active_samples(const float* sup, int64_t ns, int64_t lds,
 
 fastron_status fastron_label_capsules(const float* pos, int64_t ldp, int64_t n, const int32_t* chain, int32_t n_chain,
                                       const double* boxes, int32_t n_cubes, float radius, int8_t* label, void* stream) {
+  NvtxRange nvtx_range_("fastron_label_capsules");
   FASTRON_REQUIRE(n >= 0, "n must be >= 0");
   FASTRON_REQUIRE(n_chain >= 0 && n_chain <= 33 && n_cubes >= 0 && n_cubes <= kMaxCubes,
                   "n_chain must be in [0,33] and n_cubes in [0,64]");
@@ -480,6 +498,7 @@ fastron_status fastron_label_capsules(const float* pos, int64_t ldp, int64_t n, 
 
 fastron_status fastron_kernel_matvec(const float* K, int64_t n, int64_t ldk, const double* alpha, double* F,
                                      void* stream) {
+  NvtxRange nvtx_range_("fastron_kernel_matvec");
   FASTRON_REQUIRE(n >= 0, "n must be >= 0");
   if (n == 0) return FASTRON_OK;
   FASTRON_REQUIRE(K && alpha && F && ldk >= n, "K, alpha, F must be non-NULL and ldk >= n");
@@ -497,6 +516,7 @@ fastron_status fastron_edge_check(const fastron_robot* robot, const float* qa, c
                                   int64_t ldq, int32_t n_interp, const float* spos, const float* alpha, int64_t ns,
                                   int64_t lds, fastron_kernel k, uint8_t* in_collision, int32_t* hit_index,
                                   void* workspace, size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_range_("fastron_edge_check");
   fastron_status s = check_robot(robot);
   if (s != FASTRON_OK) return s;
   s = check_kernel(k);
@@ -570,6 +590,7 @@ size_t fastron_score_joint_workspace_bytes(int64_t nq, int64_t ns, int32_t dof) 
 fastron_status fastron_score_joint(const float* q, int64_t nq, int64_t ldq, const float* sx, const float* alpha,
                                    int64_t ns, int64_t lds, int32_t dof, fastron_kernel k, float* score,
                                    int8_t* label, void* workspace, size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_range_("fastron_score_joint");
   fastron_status s = check_kernel(k);
   if (s != FASTRON_OK) return s;
   FASTRON_REQUIRE(nq >= 0 && ns >= 0, "nq and ns must be >= 0");
@@ -613,6 +634,7 @@ size_t fastron_gram_joint_workspace_bytes(int64_t n, int32_t dof) {
 
 fastron_status fastron_gram_joint(const float* x, int64_t n, int64_t ldx, int32_t dof, fastron_kernel k, float* K,
                                   int64_t ldk, void* workspace, size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_range_("fastron_gram_joint");
   fastron_status s = check_kernel(k);
   if (s != FASTRON_OK) return s;
   FASTRON_REQUIRE(n >= 0, "n must be >= 0");
@@ -649,6 +671,7 @@ size_t fastron_query_workspace_bytes(int64_t nq, int64_t ns, int32_t n_cp, int32
 fastron_status fastron_query(const fastron_robot* robot, const float* q, int64_t nq, int64_t ldq, const float* spos,
                              const float* alpha, int64_t ns, int64_t lds, fastron_kernel k, float* score,
                              int8_t* label, void* workspace, size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_range_("fastron_query");
   fastron_status s = check_robot(robot);
   if (s != FASTRON_OK) return s;
   s = check_kernel(k);

@@ -72,6 +72,38 @@ class FastronModel:
         """X: (N, D) float32 device configurations, y: (N,) int8 device labels (+1 = C_obs)."""
         return self._train(X, y)
 
+    # ---- checkpoint / resume (loadPreviousModel, PAPER.md:219) ----
+    def state_dict(self) -> dict:
+        """The trained model: support configurations, their fp64 weights and labels, and the
+        kernel/training settings (the robot is the caller's; it is stored as its D-H table)."""
+        import torch
+        return {"supports": self.supports.cpu(), "alpha": self.alpha.cpu(), "labels": self.labels.cpu(),
+                "kind": self.kind, "gamma": self.gamma, "beta": self.beta,
+                "robot_dh": torch.as_tensor(np.asarray(self.robot.dh, dtype=np.float32)),
+                "robot_cp_frame": torch.as_tensor(np.asarray(self.robot.cp_frame, dtype=np.int32)),
+                "robot_cp_offset": torch.as_tensor(np.asarray(self.robot.cp_offset, dtype=np.float32)),
+                "robot_base": torch.as_tensor(np.asarray(self.robot.base, dtype=np.float32))}
+
+    def save(self, path: str) -> None:
+        import torch
+        torch.save(self.state_dict(), path)
+
+    def load_state_dict(self, st: dict, device="cuda") -> None:
+        """Restore a saved model (its robot must match this model's) and re-pack it."""
+        dh = np.asarray(self.robot.dh, dtype=np.float32)
+        if not np.array_equal(st["robot_dh"].numpy(), dh) or \
+                not np.array_equal(st["robot_cp_frame"].numpy(), np.asarray(self.robot.cp_frame, dtype=np.int32)):
+            raise ValueError("the saved model belongs to a different robot")
+        self.kind, self.gamma, self.beta = int(st["kind"]), float(st["gamma"]), float(st["beta"])
+        self.supports = st["supports"].to(device).contiguous()
+        self.alpha = st["alpha"].to(device).contiguous()
+        self.labels = st["labels"].to(device).contiguous()
+        self._pack()
+
+    def load(self, path: str, device="cuda") -> None:
+        import torch
+        self.load_state_dict(torch.load(path, weights_only=True), device)
+
     # ---- proxy collision check (PAPER.md:183) ----
     def query(self, q):
         qpos = fastron_fk(self.robot_c, q)

@@ -50,3 +50,27 @@ def test_fit_then_query_matches_oracle(kind):
     F = r["F"]
     sure = np.abs(F) > 1e-3
     assert np.array_equal(np.sign(s_tr.cpu().numpy()[sure]), np.sign(F[sure]))
+
+
+def test_save_load_round_trip(tmp_path):
+    """Checkpoint / resume (loadPreviousModel): a saved and re-loaded model
+    scores identically, and continues with update() from the loaded weights."""
+    require_gpu()
+    import torch
+    from paper_1910_06451_b200.model import FastronModel
+    tw = W.train_workload(600)
+    y = W.capsule_aabb_labels(W.chain_points(oracle.fk(tw.robot, tw.X)), tw.cubes, tw.radius)
+    m = FastronModel(tw.robot, kind=0, gamma=tw.gamma, iter_max=2000)
+    m.fit(dev(tw.X), dev(y))
+    path = str(tmp_path / "fastron.pt")
+    m.save(path)
+    m2 = FastronModel(tw.robot)
+    m2.load(path)
+    q = dev(W.uniform_configs(np.random.default_rng(3), 5000, 7))
+    s1, l1 = m.query(q)
+    s2, l2 = m2.query(q)
+    torch.cuda.synchronize()
+    assert torch.equal(s1, s2) and torch.equal(l1, l2)
+    assert torch.equal(m.alpha, m2.alpha) and m2.kind == 0 and m2.gamma == tw.gamma
+    with pytest.raises(ValueError):
+        FastronModel(W.arm7(16)).load(path)
