@@ -79,6 +79,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // The RBF terms of control points (m, m+1) for one (query, support) pair.
 // Gaussian: d2 = dx*dx; d2 = fma(dy,dy,d2); d2 = fma(dz,dz,d2); t = 2^-d2
 // RQ:       w = fma(dx,dx,1); w = fma(dy,dy,w); w = fma(dz,dz,w); t = rcp(w*w)
+// (the kernels accumulate through accum_term below, which evaluates RQ as rcp(w)^2)
 template <int KIND>
 __device__ __forceinline__ f2 term_from_diffs(f2 dx, f2 dy, f2 dz) {
   if (KIND == kGaussian) {
@@ -99,6 +100,28 @@ __device__ __forceinline__ f2 term_from_diffs(f2 dx, f2 dy, f2 dz) {
 template <int KIND>
 __device__ __forceinline__ f2 term_pair(f2 ux, f2 uy, f2 uz, f2 vx, f2 vy, f2 vz) {
   return term_from_diffs<KIND>(sub2(ux, vx), sub2(uy, vy), sub2(uz, vz));
+}
+
+// acc (+)= the terms of control points (m, m+1): the per-lane running sum over the pairs
+// p = 0, 1, ... (first: p == 0). Every kernel accumulates through this one function, so
+// the Gram, the scores and the lazy columns stay bit-identical.
+// Gaussian: t = 2^-d2 as above, then acc + t.
+// RQ: r = rcp(w) with w = 1 + d2, and acc = fma(r, r, acc): the square of (1 + d2)^-1 rides
+// in the accumulating FFMA2, one packed op fewer than rcp(w*w) + add (7 per pair, as the
+// Gaussian, instead of 8: the FMA pipe no longer co-limits with the MUFU).
+template <int KIND>
+__device__ __forceinline__ void accum_term(f2& acc, f2 dx, f2 dy, f2 dz, bool first) {
+  if (KIND == kGaussian) {
+    const f2 t = term_from_diffs<KIND>(dx, dy, dz);
+    acc = first ? t : add2(acc, t);
+  } else {
+    const f2 one = pk(1.0f, 1.0f);
+    f2 w = fma2(dx, dx, one);
+    w = fma2(dy, dy, w);
+    w = fma2(dz, dz, w);
+    const f2 r = pk(rcp_approx(lo(w)), rcp_approx(hi(w)));
+    acc = first ? mul2(r, r) : fma2(r, r, acc);
+  }
 }
 
 // Sum over the M control points of one (query, support) pair, in the fixed order

@@ -169,8 +169,7 @@ __global__ void __launch_bounds__(kGT, gram_min_blocks(MP))
             acc[qq][h] = fma2(dy[h], dy[h], acc[qq][h]);
             acc[qq][h] = fma2(dz[h], dz[h], acc[qq][h]);
           } else {
-            const f2 t = term_from_diffs<KIND>(dx[h], dy[h], dz[h]);
-            acc[qq][h] = p == 0 ? t : add2(acc[qq][h], t);
+            accum_term<KIND>(acc[qq][h], dx[h], dy[h], dz[h], p == 0);
           }
         }
       }

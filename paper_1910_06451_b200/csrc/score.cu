@@ -310,14 +310,12 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
         for (int j = 0; j < QT; ++j) dz[j] = sub2(uz[j][p], vz);
 #pragma unroll
         for (int j = 0; j < QT; ++j) {
-          const f2 t = term_from_diffs<KIND>(dx[j], dy[j], dz[j]);
-          acc[j] = p == 0 ? t : add2(acc[j], t);
+          accum_term<KIND>(acc[j], dx[j], dy[j], dz[j], p == 0);
         }
 #else
 #pragma unroll
         for (int j = 0; j < QT; ++j) {
-          const f2 t = term_pair<KIND>(ux[j][p], uy[j][p], uz[j][p], vx, vy, vz);
-          acc[j] = p == 0 ? t : add2(acc[j], t);
+          accum_term<KIND>(acc[j], sub2(ux[j][p], vx), sub2(uy[j][p], vy), sub2(uz[j][p], vz), p == 0);
         }
 #endif
       }

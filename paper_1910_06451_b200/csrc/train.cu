@@ -447,8 +447,7 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
             const f2 ux = s_pts[(int64_t)(p * 3 + 0) * A.chunk + koff[k]];
             const f2 uy = s_pts[(int64_t)(p * 3 + 1) * A.chunk + koff[k]];
             const f2 uz = s_pts[(int64_t)(p * 3 + 2) * A.chunk + koff[k]];
-            const f2 t = term_pair<LKIND>(ux, uy, uz, vx[p], vy[p], vz[p]);
-            acc = p == 0 ? t : add2(acc, t);
+            accum_term<LKIND>(acc, sub2(ux, vx[p]), sub2(uy, vy[p]), sub2(uz, vz[p]), p == 0);
           }
           const float ks = pair_sum(acc);
           const float v = A.m_pow2 ? ks * A.inv_m : __fdiv_rn(ks, (float)A.M);
