@@ -14,11 +14,12 @@ c = f32(np.sqrt(g / 2))
 S = (sp.astype(f32) * c).astype(f32)
 
 
-def lanes32(t):  # even / odd control points summed in fp32, then promoted
-    t = t.astype(f32)
-    l0, l1 = t[:, 0], t[:, 1]
-    for m in range(2, t.shape[1], 2):
-        l0, l1 = (l0 + t[:, m]).astype(f32), (l1 + t[:, m + 1]).astype(f32)
+def lanes32(r):  # even / odd lanes: acc = fma(r, r, acc) in fp32 (one rounding), then promoted
+    r = r.astype(np.float64)
+    l0, l1 = (r[:, 0] * r[:, 0]).astype(f32), (r[:, 1] * r[:, 1]).astype(f32)
+    for m in range(2, r.shape[1], 2):
+        l0 = (r[:, m] * r[:, m] + l0.astype(np.float64)).astype(f32)
+        l1 = (r[:, m + 1] * r[:, m + 1] + l1.astype(np.float64)).astype(f32)
     return l0.astype(np.float64) + l1.astype(np.float64)
 
 
@@ -34,10 +35,11 @@ for i in range(NQ):
     d2 = (d2 + (d[..., 1] * d[..., 1]).astype(f32)).astype(f32)
     d2 = (d2 + (d[..., 2] * d[..., 2]).astype(f32)).astype(f32)
     w = (f32(1) + d2).astype(f32)
-    t = (f32(1) / (w * w).astype(f32)).astype(f32)
-    M = t.shape[1]
+    r = (f32(1) / w).astype(f32)  # the kernel: r = rcp(1 + d2), terms r^2 fused into the lane sums
+    M = r.shape[1]
+    t = (r.astype(np.float64) ** 2).astype(f32)
     err["+ fp32 term arithmetic (fp64 sums)"].append((a * t.astype(np.float64).sum(-1)).sum() / M - ref)
-    err["+ fp32 lane sums (kernel)"].append((a * lanes32(t)).sum() / M - ref)
+    err["+ fp32 lane sums (kernel)"].append((a * lanes32(r)).sum() / M - ref)
 for k, v in err.items():
     v = np.abs(np.array(v))
     print(f"{k:40s} rms {np.sqrt((v ** 2).mean()):.2e}  max {v.max():.2e}")
