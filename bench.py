@@ -566,6 +566,19 @@ def main():
     ap.add_argument("--rows", action="store_true", help="also time cfg1/cfg2/cfg3/cfg4 rows")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` without a launcher: start one rank per GPU ourselves,
+        # exactly as the driver does (torchrun, rendezvous on 127.0.0.1)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.execv(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                  f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+                                  str(port), os.path.abspath(__file__)] + sys.argv[1:])
+    ws_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws_env != args.gpus:
+        print(f"note: --gpus {args.gpus} but WORLD_SIZE={ws_env}; reporting n_gpus={ws_env}", file=sys.stderr)
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
         args.warmup = 3
