@@ -122,6 +122,7 @@ def cpu_baseline(wl, target_s=12.0):
     """The oracle as it stands, on this host's cores, on a bounded sample of the workload:
     the first Qs queries of the batch against all supports (FK + fp64 score)."""
     import oracle
+    oracle.set_num_threads(os.cpu_count() or 1)  # all host cores (torchrun sets OMP_NUM_THREADS=1)
     spos = oracle.fk(wl.robot, wl.supports)
 
     def run(nq):
@@ -154,6 +155,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     import oracle
+    oracle.set_num_threads(os.cpu_count() or 1)  # all host cores (torchrun sets OMP_NUM_THREADS=1)
     wl = W.score_workload("headline", kind=args.kind)
     spos = oracle.fk(wl.robot, wl.supports)
     # each step: a bounded sample of the batch (a different slice per step)
