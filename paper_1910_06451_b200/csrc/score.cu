@@ -118,6 +118,14 @@ struct ScoreArgs {
   int64_t plan_nq;  // host only: batch size the split count is planned for (0: nq)
 };
 
+// Final write of one query's fp64 sum: 1/denom, fp64 / fp32 score, label (R8).
+__device__ __forceinline__ void write_score(const ScoreArgs& A, int64_t vq, double f) {
+  const double fm = f / A.denom;
+  if (A.score64) A.score64[vq] = fm;
+  if (A.score) A.score[vq] = (float)fm;
+  if (A.label) A.label[vq] = fm > 0.0 ? 1 : -1;
+}
+
 // Position k of the visiting order of round r, lane l: evens first, then odds (R11).
 __device__ __forceinline__ int edge_point(int n_interp, int o) {
   const int n_even = (n_interp + 1) >> 1;
@@ -380,6 +388,111 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ S
 }
 
 // ---------------------------------------------------------------------------------
+// small batches (nq <= kSmallQ): support-parallel scoring
+// ---------------------------------------------------------------------------------
+// The tile kernel gives every CTA 128*QT query slots, so a planner asking for one
+// configuration would run 512 slots per CTA for one live query. Here each thread owns
+// supports (grid-stride), the <= 32 queries sit in shared memory, and every thread keeps
+// one fp64 partial per query; the CTA reduces them in a fixed order, and the last CTA to
+// finish (ticket counter) adds the CTA partials in CTA order: one launch, deterministic.
+// Terms, lane sums and fp64 accumulation are those of K2 (same tolerance).
+constexpr int kSmallQ = 32;
+constexpr int kSmallNT = 256;
+
+template <int MP, int KIND>
+__global__ void __launch_bounds__(kSmallNT) score_small_kernel(const __grid_constant__ ScoreArgs A, int64_t ns,
+                                                               unsigned int* __restrict__ ticket) {
+  constexpr int NP = MP / 2;
+  constexpr int64_t TF = tile_floats(MP);
+  __shared__ f2 sq[kSmallQ][NP][3];
+  __shared__ double s_red[kSmallNT / 32][kSmallQ];
+  __shared__ int s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nq = (int)A.nq;
+  for (int i = tid; i < nq * NP; i += kSmallNT) {  // queries -> scaled pairs (padded point: 0)
+    const int q = i / NP, p = i % NP;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    if (2 * p < A.M) a = __ldg(A.qpos + (int64_t)(2 * p) * A.ldq + q);
+    if (2 * p + 1 < A.M) b = __ldg(A.qpos + (int64_t)(2 * p + 1) * A.ldq + q);
+    sq[q][p][0] = pk(__fmul_rn(a.x, A.scale), __fmul_rn(b.x, A.scale));
+    sq[q][p][1] = pk(__fmul_rn(a.y, A.scale), __fmul_rn(b.y, A.scale));
+    sq[q][p][2] = pk(__fmul_rn(a.z, A.scale), __fmul_rn(b.z, A.scale));
+  }
+  __syncthreads();
+  double f[kSmallQ];
+#pragma unroll
+  for (int q = 0; q < kSmallQ; ++q) f[q] = 0.0;
+  for (int64_t sup = (int64_t)blockIdx.x * kSmallNT + tid; sup < ns; sup += (int64_t)gridDim.x * kSmallNT) {
+    const float* T = A.packed + (sup / kTileSupports) * TF;
+    const float* rec = T + (sup % kTileSupports) * NP * 8;
+    const double a = reinterpret_cast<const double*>(T + tile_record_floats(MP))[sup % kTileSupports];
+    f2 vx[NP], vy[NP], vz[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const float4 xy = __ldg(reinterpret_cast<const float4*>(rec + p * 8));
+      const float2 zz = __ldg(reinterpret_cast<const float2*>(rec + p * 8 + 4));
+      vx[p] = pk(xy.x, xy.y);
+      vy[p] = pk(xy.z, xy.w);
+      vz[p] = pk(zz.x, zz.y);
+    }
+#pragma unroll
+    for (int q = 0; q < kSmallQ; ++q) {
+      if (q < nq) {  // uniform
+        f2 acc;
+#pragma unroll
+        for (int p = 0; p < NP; ++p)
+          accum_term<KIND>(acc, sub2(sq[q][p][0], vx[p]), sub2(sq[q][p][1], vy[p]), sub2(sq[q][p][2], vz[p]), p == 0);
+        f[q] = fma(a, nonneg_f32_to_f64(lo(acc)), f[q]);
+        f[q] = fma(a, nonneg_f32_to_f64(hi(acc)), f[q]);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kSmallQ; ++q) {
+    if (q < nq) {
+      double v = f[q];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+      if (lane == 0) s_red[warp][q] = v;
+    }
+  }
+  __syncthreads();
+  if (tid < nq) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < kSmallNT / 32; ++w) v += s_red[w][tid];
+    A.partial[(int64_t)blockIdx.x * kSmallQ + tid] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (tid < nq) {
+    double v = 0.0;
+    for (unsigned c = 0; c < gridDim.x; ++c) v += __ldcg(A.partial + (int64_t)c * kSmallQ + tid);
+    write_score(A, tid, v);
+  }
+  if (tid == 0) *ticket = 0u;  // reset for the next call on this workspace
+}
+
+template <int MP, int KIND>
+static cudaError_t run_score_small(const ScoreArgs& A, int64_t ns, cudaStream_t st) {
+  const int64_t want = (ns + kSmallNT - 1) / kSmallNT;
+  const int64_t grid = want < 1 ? 1 : (want > device_info().sms ? device_info().sms : want);
+  // partials: [grid][kSmallQ] doubles; the ticket counter follows them
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(A.partial + (int64_t)device_info().sms * kSmallQ);
+  cudaError_t e = cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st);
+  if (e != cudaSuccess) return e;
+  score_small_kernel<MP, KIND><<<(unsigned)grid, kSmallNT, 0, st>>>(A, ns, ticket);
+  g_launches.fetch_add(1);
+  return cudaGetLastError();
+}
+
+size_t score_small_bytes() { return (size_t)device_info().sms * kSmallQ * sizeof(double) + 256; }
+
+// ---------------------------------------------------------------------------------
 // planning + dispatch
 // ---------------------------------------------------------------------------------
 // Support splits. Measured on the headline (tools/split_probe.sh): the time falls as the
@@ -411,7 +524,9 @@ int score_max_splits(int64_t nq, int64_t ns, int M) {
 
 size_t score_partial_bytes(int64_t nq, int64_t ns, int M) {
   const int s = score_max_splits(nq, ns, M);
-  return s > 1 ? (size_t)s * (size_t)nq * sizeof(double) : 0;
+  const size_t tiles = s > 1 ? (size_t)s * (size_t)nq * sizeof(double) : 0;
+  const size_t small = (nq > 0 && nq <= kSmallQ && M <= 16) ? score_small_bytes() : 0;
+  return tiles > small ? tiles : small;
 }
 
 template <int MP, int KIND, int MODE>
@@ -579,6 +694,26 @@ cudaError_t launch_score(const float4* qpos, int64_t nq, int64_t ldq, const floa
   A.partial = partial;
   A.denom = (double)M;
   FkParams P = {};
+  // a small batch (planned as a whole) takes the support-parallel kernel
+  const int64_t batch = plan_nq > nq ? plan_nq : nq;
+  if (batch <= kSmallQ && ns > 0 && M <= 16 && partial) {
+    switch (padded_m(M)) {
+#define FASTRON_SCASE(mp)                                                                            \
+  case mp:                                                                                           \
+    return kind == kGaussian ? run_score_small<mp, kGaussian>(A, ns, st) : run_score_small<mp, kRQ>(A, ns, st);
+      FASTRON_SCASE(2)
+      FASTRON_SCASE(4)
+      FASTRON_SCASE(6)
+      FASTRON_SCASE(8)
+      FASTRON_SCASE(10)
+      FASTRON_SCASE(12)
+      FASTRON_SCASE(14)
+      FASTRON_SCASE(16)
+#undef FASTRON_SCASE
+      default:
+        break;
+    }
+  }
   return dispatch<MODE_POS>(A, P, nq, ns, kind, st);
 }
 

@@ -208,3 +208,39 @@ def test_query_chunks_planned_like_the_batch():
     lh = torch.empty(len(wl.queries), dtype=torch.int8).pin_memory()
     fb.fastron_query(wl.robot, qh, spos, alpha, 0, wl.gamma, score=sh, label=lh)
     assert np.array_equal(sh.numpy(), s_dev) and np.array_equal(lh.numpy(), l_dev)
+
+
+@pytest.mark.parametrize("M", [4, 5, 8, 16])
+@pytest.mark.parametrize("kind", [W.GAUSSIAN, W.RQ])
+def test_small_batches(M, kind):
+    """nq <= 32 takes the support-parallel kernel (one launch, fixed-order reduction):
+    parity for 1..32 queries against 1 to 20,000 supports, and every path agrees with it."""
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    base = W.arm7(8)
+    rng = np.random.default_rng(40 + M)
+    robot = base if M == 8 else W.make_robot("m%d" % M, base.dh, rng.integers(1, 8, size=M),
+                                              rng.uniform(-0.1, 0.1, size=(M, 3)))
+    sup = W.uniform_configs(rng, 20_000, 7)
+    alpha = rng.standard_normal(20_000).astype(np.float32)
+    q = W.uniform_configs(rng, 32, 7)
+    spos_ref = oracle.fk(robot, sup)
+    qpos_ref = oracle.fk(robot, q)
+    for ns in (1, 63, 303, 20_000):
+        for nq in (1, 5, 32):
+            s, l = _gpu_scores(robot, sup[:ns], alpha[:ns], q[:nq], kind, 5.0)
+            f, _ = oracle.score(kind, 5.0, qpos_ref[:nq], spos_ref[:ns], alpha[:ns])
+            floor = 1e-5 if kind == W.GAUSSIAN else rq_floor(ns)
+            assert_score_parity(s, f, l, floor=floor, what=f"small M={M} kind={kind} ns={ns} nq={nq}")
+    # the packed-model path, the fp64 path and fastron_query give the same small-batch scores
+    spos = fb.fastron_fk(robot, dev(sup))
+    model = fb.fastron_model_pack(spos, dev(alpha), kind, 5.0)
+    qpos = fb.fastron_fk(robot, dev(q[:7]))
+    s1, _ = fb.fastron_score_packed(qpos, model)
+    s64 = fb.fastron_score_packed_f64(qpos, model)
+    sh = torch.empty(7, dtype=torch.float32).pin_memory()
+    fb.fastron_query(robot, torch.from_numpy(q[:7].copy()), spos, dev(alpha), kind, 5.0, score=sh)
+    torch.cuda.synchronize()
+    assert np.array_equal(s1.cpu().numpy(), sh.numpy())
+    assert np.array_equal(s1.cpu().numpy(), s64.cpu().numpy().astype(np.float32))
