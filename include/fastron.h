@@ -113,7 +113,12 @@ fastron_status fastron_fk(const fastron_robot* robot, const float* q, int64_t n,
  *   workspace: device scratch of >= fastron_score_workspace_bytes(nq, ns, n_cp) bytes,
  *   256-byte aligned; contents are overwritten.
  * ns == 0 gives f = 0, label -1. nq == 0 is a no-op.
- * Results are deterministic (fixed-order reductions) for a given device.
+ * Results are deterministic (fixed-order reductions) for a given device and batch size;
+ * the fp64 summation order follows the batch: nq <= 32 (n_cp <= 16) runs a
+ * support-parallel kernel, larger batches split the supports over a number of CTAs
+ * chosen from nq, so the same query may differ in the last fp32 bit between batches of
+ * different sizes (always within the tolerance of DESIGN.md R16). The workspace also
+ * carries a completion counter: one call at a time per workspace.
  */
 size_t fastron_score_workspace_bytes(int64_t nq, int64_t ns, int32_t n_cp);
 fastron_status fastron_score(const float* qpos, int64_t nq, int64_t ldq, const float* spos, const float* alpha,
