@@ -74,3 +74,23 @@ def test_save_load_round_trip(tmp_path):
     assert torch.equal(m.alpha, m2.alpha) and m2.kind == 0 and m2.gamma == tw.gamma
     with pytest.raises(ValueError):
         FastronModel(W.arm7(16)).load(path)
+
+
+def test_query_graph_matches_query():
+    """A captured fixed-size query (CUDA graph replay) returns the same scores and labels as
+    the launch-by-launch query, for successive different inputs."""
+    require_gpu()
+    import torch
+    from paper_1910_06451_b200.model import FastronModel
+    tw = W.train_workload(500)
+    y = W.capsule_aabb_labels(W.chain_points(oracle.fk(tw.robot, tw.X)), tw.cubes, tw.radius)
+    m = FastronModel(tw.robot, kind=0, gamma=tw.gamma, iter_max=1000)
+    m.fit(dev(tw.X), dev(y))
+    for nq in (1, 32, 1000):
+        run = m.query_graph(nq)
+        for seed in (1, 2):
+            q = dev(W.uniform_configs(np.random.default_rng(seed), nq, 7))
+            s_ref, l_ref = m.query(q)
+            s, l = run(q)
+            torch.cuda.synchronize()
+            assert torch.equal(s, s_ref) and torch.equal(l, l_ref)
