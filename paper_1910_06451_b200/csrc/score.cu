@@ -31,6 +31,10 @@ namespace fastron {
 #ifndef FASTRON_ACC_SPLIT
 #define FASTRON_ACC_SPLIT 1
 #endif
+#ifndef FASTRON_SUP_UNROLL
+#define FASTRON_SUP_UNROLL 2
+#endif
+constexpr int kSupUnroll = FASTRON_SUP_UNROLL;  // supports per unrolled step of K2's inner loop
 
 constexpr int kNT = 128;     // threads per scoring CTA
 constexpr int kStages = 3;   // TMA ring depth
@@ -266,7 +270,7 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
     mbar_wait(&bars[st], (uint32_t)((it / kStages) & 1));
     const float* T = stages + st * TF;
     const double* alpha = reinterpret_cast<const double*>(T + tile_record_floats(MP));
-#pragma unroll 2
+#pragma unroll kSupUnroll
     for (int s = 0; s < kTileSupports; ++s) {
       const float* rec = T + s * NP * 8;
       const double a = alpha[s];
