@@ -36,8 +36,14 @@ namespace fastron {
 #endif
 constexpr int kSupUnroll = FASTRON_SUP_UNROLL;  // supports per unrolled step of K2's inner loop
 
-constexpr int kNT = 128;     // threads per scoring CTA
-constexpr int kStages = 3;   // TMA ring depth
+#ifndef FASTRON_SCORE_NT
+#define FASTRON_SCORE_NT 128
+#endif
+#ifndef FASTRON_SCORE_STAGES
+#define FASTRON_SCORE_STAGES 3
+#endif
+constexpr int kNT = FASTRON_SCORE_NT;  // threads per scoring CTA
+constexpr int kStages = FASTRON_SCORE_STAGES;  // TMA ring depth
 
 __host__ __device__ constexpr int qt_for(int mp) { return mp <= 4 ? 8 : mp <= 8 ? 4 : mp <= 16 ? 2 : 1; }
 
