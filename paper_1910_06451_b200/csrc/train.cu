@@ -683,6 +683,13 @@ cudaError_t launch_train(const float* K, int64_t n, int64_t ldk, const int8_t* y
                          cudaStream_t st) {
   int C = (int)((n + kChunkMax - 1) / kChunkMax);
   if (C < 1) C = 1;
+  // Above one CTA the winner exchange is paid anyway, and smaller slices shorten the scan:
+  // ~1,024 points per CTA (tools/train_big_probe.py: N = 8,446 C = 2 1.76, 4 1.59, 9 1.43,
+  // 16 1.46 us / iteration; N = 20,000 C = 4 2.00, 8 1.83, 12 1.76, 16 1.77).
+  if (C > 1) {
+    const int c_small = (int)((n + 1023) / 1024);
+    C = c_small > C ? (c_small < kMaxCluster ? c_small : kMaxCluster) : C;
+  }
   if (const char* env = getenv("FASTRON_TRAIN_CLUSTER")) {  // tuning override (>= the minimum)
     const int c = atoi(env);
     if (c > C) C = c;
@@ -750,6 +757,10 @@ cudaError_t launch_train_lazy(const float* packed, int64_t n, int M, int kind, c
   if (chunk_max > 4 * kTrainNT) chunk_max = 4 * kTrainNT;
   int C = (int)((n + chunk_max - 1) / chunk_max);
   if (C < 1) C = 1;
+  if (C > 1) {  // as in launch_train: ~1,024 points per CTA once the exchange is paid
+    const int c_small = (int)((n + 1023) / 1024);  // (lazy cfg3: C = 3 1.62, 5 1.43, 8 1.46 us)
+    C = c_small > C ? (c_small < kMaxCluster ? c_small : kMaxCluster) : C;
+  }
   if (const char* env = getenv("FASTRON_TRAIN_CLUSTER")) {
     const int c = atoi(env);
     if (c > C) C = c;
