@@ -164,7 +164,8 @@ fastron_status fastron_gram(const float* pos, int64_t n, int64_t ldp, int32_t n_
 
 /*
  * fastron_train — Algorithm 1, "Fastron Model Update Algorithm" (PAPER.md:206-252,
- * Eq. 6-9), run entirely on the device in one persistent cluster kernel.
+ * Eq. 6-9), run entirely on the device in one persistent cluster kernel (one CTA up to
+ * 6,144 points; above, a cluster of ~n/1024 CTAs up to 16, chosen by the library).
  *   K: device float [n][ldk] Gram (from fastron_gram; promoted to fp64 on read).
  *   y: device int8 [n], +1 = C_obs, -1 = C_free.
  *   beta >= 1: conditional bias, b_i = beta^(0.5 (y_i + 1)).
@@ -197,7 +198,7 @@ fastron_status fastron_train(const float* K, int64_t n, int64_t ldk, const int8_
  * read it back. Columns are bit-identical to fastron_gram's, so the result equals
  * fastron_train(fastron_gram(pos)) exactly.
  *   pos: device float4 [n_cp][ldp] control points of the n training configurations;
- *   k: the FK-kernel term (n_cp in {1..4, 7, 8, 15, 16}: padded to 4, 8 or 16);
+ *   k: the FK-kernel term; n_cp <= 16 (odd n_cp padded as in fastron_score);
  *   y, beta, iter_max, s_max, alpha_inout, F_inout, support_idx, trace, result: as
  *   fastron_train. cache_cols >= 0 (columns beyond the cache are recomputed).
  *   workspace: >= fastron_train_lazy_workspace_bytes(n, n_cp, cache_cols).
