@@ -153,8 +153,8 @@ fastron_status fastron_score_packed(const float* qpos, int64_t nq, int64_t ldq, 
 /*
  * fastron_gram — FK-kernel Gram matrix K_ij = K_FK(X_i, X_j),
  * written in full (both triangles; computed once per unordered pair and mirrored,
- * so K is exactly symmetric, and K_ii = 1 exactly for n_cp a power of two).
- * Values are bit-identical to fastron_score with alpha = e_i.
+ * so K is exactly symmetric), K_ii = 1 exactly. For n_cp a power of two the values are
+ * bit-identical to fastron_score with alpha = e_i.
  *   pos: device float4 [n_cp][ldp], ldp >= n. K: device float [n][ldk], ldk >= n.
  *   workspace: >= fastron_gram_workspace_bytes(n, n_cp).
  */
