@@ -373,6 +373,7 @@ def _time_rows(fb, torch, kind):
     # FK + score for nq queries, stream launches vs a captured CUDA graph, at the Table I
     # FK model size (|S| = 303) and the headline model (|S| = 20,000)
     lat = {}
+    robot_c = fb.make_robot_struct(hw.robot)
     for ns in (303, 20_000):
         sp = fb.fastron_fk(hw.robot, torch.from_numpy(hw.supports[:ns]).cuda())
         mdl = fb.fastron_model_pack(sp, torch.from_numpy(hw.alpha[:ns]).cuda(), kind, hw.gamma)
@@ -385,6 +386,15 @@ def _time_rows(fb, torch, kind):
                               dtype=torch.uint8, device="cuda")
             fn = lambda: (fb.fastron_fk(hw.robot, qs, pos=qp), fb.fastron_score_packed(qp, mdl, sc, lb, workspace=wsl))
             lat[f"S{ns}_q{nq}"] = {"stream_us": timed(fn, 200) * 1e3, "graph_us": graphed(fn, 200) * 1e3}
+            if nq <= 32:  # fastron_query on device buffers: one fused launch for small batches
+                sp_ = sp.contiguous()
+                al_ = torch.from_numpy(hw.alpha[:ns]).cuda()
+                qws_ = torch.empty(fb.load_library().fastron_query_workspace_bytes(nq, ns, 8, 7), dtype=torch.uint8,
+                                   device="cuda")
+                fq = lambda: fb.fastron_query(robot_c, qs, sp_, al_, kind, hw.gamma, score=sc, label=lb,
+                                              workspace=qws_)
+                lat[f"S{ns}_q{nq}"]["query_stream_us"] = timed(fq, 200) * 1e3
+                lat[f"S{ns}_q{nq}"]["query_graph_us"] = graphed(fq, 200) * 1e3
     rows["small_batch_latency"] = lat
     # cfg4: 10k edges x 64 points, 3k supports, early exit
     ew = W.edge_workload()

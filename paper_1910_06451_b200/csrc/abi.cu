@@ -731,10 +731,14 @@ fastron_status fastron_query(const fastron_robot* robot, const float* q, int64_t
     // device pointers: FK of the whole batch through the positions buffer in chunks
     for (int64_t off = 0; off < nq; off += chunk) {
       const int64_t n = nq - off < chunk ? nq - off : chunk;
-      e = launch_fk(P, q + off * ldq, n, ldq, reinterpret_cast<float4*>(buf[0].pos), chunk, st);
-      if (e == cudaSuccess)
-        e = launch_score(reinterpret_cast<const float4*>(buf[0].pos), n, chunk, packed, ns, M, k.kind, c,
-                         score ? score + off : nullptr, label ? label + off : nullptr, partial, st, nullptr, nq);
+      if (query_small_ok(nq, ns, M)) {  // one launch: FK inside the small-batch kernel
+        e = launch_query_small(P, q, nq, ldq, packed, ns, M, k.kind, c, score, label, partial, st);
+      } else {
+        e = launch_fk(P, q + off * ldq, n, ldq, reinterpret_cast<float4*>(buf[0].pos), chunk, st);
+        if (e == cudaSuccess)
+          e = launch_score(reinterpret_cast<const float4*>(buf[0].pos), n, chunk, packed, ns, M, k.kind, c,
+                           score ? score + off : nullptr, label ? label + off : nullptr, partial, st, nullptr, nq);
+      }
       if (e != cudaSuccess) return cuda_status(e, "fastron_query");
     }
     return FASTRON_OK;
@@ -773,10 +777,14 @@ fastron_status fastron_query(const fastron_robot* robot, const float* q, int64_t
     cudaStreamWaitEvent(cs[b], ev_out[b], 0);
     float* sdev = score ? (s_host ? buf[b].sc : score + off) : nullptr;
     int8_t* ldev = label ? (l_host ? buf[b].lb : label + off) : nullptr;
-    if (e == cudaSuccess) e = launch_fk(P, qdev, n, ldq_dev, reinterpret_cast<float4*>(buf[b].pos), chunk, cs[b]);
-    if (e == cudaSuccess)
-      e = launch_score(reinterpret_cast<const float4*>(buf[b].pos), n, chunk, packed, ns, M, k.kind, c, sdev, ldev,
-                       partials[b], cs[b], nullptr, nq);
+    if (e == cudaSuccess && query_small_ok(nq, ns, M)) {  // one launch: FK inside the small-batch kernel
+      e = launch_query_small(P, qdev, n, ldq_dev, packed, ns, M, k.kind, c, sdev, ldev, partials[b], cs[b]);
+    } else {
+      if (e == cudaSuccess) e = launch_fk(P, qdev, n, ldq_dev, reinterpret_cast<float4*>(buf[b].pos), chunk, cs[b]);
+      if (e == cudaSuccess)
+        e = launch_score(reinterpret_cast<const float4*>(buf[b].pos), n, chunk, packed, ns, M, k.kind, c, sdev, ldev,
+                         partials[b], cs[b], nullptr, nq);
+    }
     cudaEventRecord(ev_used[b], cs[b]);
     // results out
     cudaStreamWaitEvent(d2h, ev_used[b], 0);

@@ -53,6 +53,13 @@ cudaError_t launch_score(const float4* qpos, int64_t nq, int64_t ldq, const floa
                          float scale, float* score, int8_t* label, double* partial, cudaStream_t st,
                          double* score64 = nullptr, int64_t plan_nq = 0);
 
+// Small fastron_query (nq <= 32, M <= 16): FK of the configurations inside the
+// support-parallel scoring kernel, one launch. partial: >= score_partial_bytes(nq, ..).
+bool query_small_ok(int64_t nq, int64_t ns, int M);
+cudaError_t launch_query_small(const FkParams& P, const float* q, int64_t nq, int64_t ldq, const float* packed,
+                               int64_t ns, int M, int kind, float scale, float* score, int8_t* label,
+                               double* partial, cudaStream_t st);
+
 // K4: one round of the fused edge check (interpolate -> FK -> score -> warp vote).
 struct EdgeRound {
   const float* qa;

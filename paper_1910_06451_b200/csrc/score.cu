@@ -126,6 +126,8 @@ struct ScoreArgs {
   double denom;  // M for the FK kernel's 1/M mean (Eq. 4), 1 for the joint-space kernel
   double* score64;  // optional fp64 scores (margins for a warm start)
   int64_t plan_nq;  // host only: batch size the split count is planned for (0: nq)
+  const float* qcfg;  // small fused query: configurations [nq][ldqc] (FK in the kernel)
+  int64_t ldqc;
 };
 
 // Final write of one query's fp64 sum: 1/denom, fp64 / fp32 score, label (R8).
@@ -409,21 +411,44 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ S
 constexpr int kSmallQ = 32;
 constexpr int kSmallNT = 256;
 
-template <int MP, int KIND>
-__global__ void __launch_bounds__(kSmallNT) score_small_kernel(const __grid_constant__ ScoreArgs A, int64_t ns,
+// FUSED_FK: the queries arrive as configurations and thread q runs the D-H chain of
+// query q (fk_chain, the FK kernel's arithmetic and rounding: the same positions), so a
+// small fastron_query is one launch.
+template <int MP, int KIND, bool FUSED_FK>
+__global__ void __launch_bounds__(kSmallNT) score_small_kernel(const __grid_constant__ ScoreArgs A,
+                                                               const __grid_constant__ FkParams P, int64_t ns,
                                                                unsigned int* __restrict__ ticket) {
   constexpr int NP = MP / 2;
   constexpr int64_t TF = tile_floats(MP);
   __shared__ f2 sq[kSmallQ][NP][3];
   __shared__ double s_red[kSmallNT / 32][kSmallQ];
+  __shared__ float s_pos[FUSED_FK ? kSmallQ : 1][FUSED_FK ? MP : 1][3];
   __shared__ int s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nq = (int)A.nq;
+  if (FUSED_FK) {
+    if (tid < nq) {
+      const float* qk = A.qcfg + (int64_t)tid * A.ldqc;
+      fk_chain(
+          P, [&](int j) { return (double)__ldg(qk + j); },
+          [&](int m, double x, double y, double z) {
+            s_pos[tid][m][0] = __double2float_rn(x);
+            s_pos[tid][m][1] = __double2float_rn(y);
+            s_pos[tid][m][2] = __double2float_rn(z);
+          });
+    }
+    __syncthreads();
+  }
   for (int i = tid; i < nq * NP; i += kSmallNT) {  // queries -> scaled pairs (padded point: 0)
     const int q = i / NP, p = i % NP;
     float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-    if (2 * p < A.M) a = __ldg(A.qpos + (int64_t)(2 * p) * A.ldq + q);
-    if (2 * p + 1 < A.M) b = __ldg(A.qpos + (int64_t)(2 * p + 1) * A.ldq + q);
+    if (FUSED_FK) {
+      if (2 * p < A.M) a = make_float4(s_pos[q][2 * p][0], s_pos[q][2 * p][1], s_pos[q][2 * p][2], 0.f);
+      if (2 * p + 1 < A.M) b = make_float4(s_pos[q][2 * p + 1][0], s_pos[q][2 * p + 1][1], s_pos[q][2 * p + 1][2], 0.f);
+    } else {
+      if (2 * p < A.M) a = __ldg(A.qpos + (int64_t)(2 * p) * A.ldq + q);
+      if (2 * p + 1 < A.M) b = __ldg(A.qpos + (int64_t)(2 * p + 1) * A.ldq + q);
+    }
     sq[q][p][0] = pk(__fmul_rn(a.x, A.scale), __fmul_rn(b.x, A.scale));
     sq[q][p][1] = pk(__fmul_rn(a.y, A.scale), __fmul_rn(b.y, A.scale));
     sq[q][p][2] = pk(__fmul_rn(a.z, A.scale), __fmul_rn(b.z, A.scale));
@@ -487,15 +512,15 @@ __global__ void __launch_bounds__(kSmallNT) score_small_kernel(const __grid_cons
   if (tid == 0) *ticket = 0u;  // reset for the next call on this workspace
 }
 
-template <int MP, int KIND>
-static cudaError_t run_score_small(const ScoreArgs& A, int64_t ns, cudaStream_t st) {
+template <int MP, int KIND, bool FUSED_FK = false>
+static cudaError_t run_score_small(const ScoreArgs& A, int64_t ns, cudaStream_t st, const FkParams& P = FkParams{}) {
   const int64_t want = (ns + kSmallNT - 1) / kSmallNT;
   const int64_t grid = want < 1 ? 1 : (want > device_info().sms ? device_info().sms : want);
   // partials: [grid][kSmallQ] doubles; the ticket counter follows them
   unsigned int* ticket = reinterpret_cast<unsigned int*>(A.partial + (int64_t)device_info().sms * kSmallQ);
   cudaError_t e = cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st);
   if (e != cudaSuccess) return e;
-  score_small_kernel<MP, KIND><<<(unsigned)grid, kSmallNT, 0, st>>>(A, ns, ticket);
+  score_small_kernel<MP, KIND, FUSED_FK><<<(unsigned)grid, kSmallNT, 0, st>>>(A, P, ns, ticket);
   g_launches.fetch_add(1);
   return cudaGetLastError();
 }
@@ -725,6 +750,41 @@ cudaError_t launch_score(const float4* qpos, int64_t nq, int64_t ldq, const floa
     }
   }
   return dispatch<MODE_POS>(A, P, nq, ns, kind, st);
+}
+
+bool query_small_ok(int64_t nq, int64_t ns, int M) { return nq > 0 && nq <= kSmallQ && ns > 0 && M <= 16; }
+
+cudaError_t launch_query_small(const FkParams& P, const float* q, int64_t nq, int64_t ldq, const float* packed,
+                               int64_t ns, int M, int kind, float scale, float* score, int8_t* label,
+                               double* partial, cudaStream_t st) {
+  ScoreArgs A = {};
+  A.qcfg = q;
+  A.ldqc = ldq;
+  A.nq = nq;
+  A.packed = packed;
+  A.M = M;
+  A.scale = scale;
+  A.score = score;
+  A.label = label;
+  A.partial = partial;
+  A.denom = (double)M;
+  switch (padded_m(M)) {
+#define FASTRON_QCASE(mp)                                                                   \
+  case mp:                                                                                  \
+    return kind == kGaussian ? run_score_small<mp, kGaussian, true>(A, ns, st, P)           \
+                             : run_score_small<mp, kRQ, true>(A, ns, st, P);
+    FASTRON_QCASE(2)
+    FASTRON_QCASE(4)
+    FASTRON_QCASE(6)
+    FASTRON_QCASE(8)
+    FASTRON_QCASE(10)
+    FASTRON_QCASE(12)
+    FASTRON_QCASE(14)
+    FASTRON_QCASE(16)
+#undef FASTRON_QCASE
+    default:
+      return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_edge_round(const FkParams& P, const EdgeRound& R, const float* packed, int64_t ns, int M, int kind,

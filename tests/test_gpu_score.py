@@ -244,3 +244,9 @@ def test_small_batches(M, kind):
     torch.cuda.synchronize()
     assert np.array_equal(s1.cpu().numpy(), sh.numpy())
     assert np.array_equal(s1.cpu().numpy(), s64.cpu().numpy().astype(np.float32))
+    # fastron_query on device buffers: FK fused into the small-batch kernel, same scores
+    sd = torch.empty(7, dtype=torch.float32, device="cuda")
+    ld = torch.empty(7, dtype=torch.int8, device="cuda")
+    fb.fastron_query(robot, dev(q[:7]), spos, dev(alpha), kind, 5.0, score=sd, label=ld)
+    torch.cuda.synchronize()
+    assert np.array_equal(s1.cpu().numpy(), sd.cpu().numpy())
