@@ -34,6 +34,7 @@ import workloads as W  # noqa: E402
 METRIC = "7-DOF FK-kernel proxy collision checks/sec (1M queries x 20k supports, M=8)"
 UNIT = "checks/s"
 MUFU_PER_CLK_PER_SM = 16  # B200 SFU: 16 ex2/rcp per clock per SM (tools/pipe_peaks.cu measured 15.8)
+MUFU_MEASURED_PER_CLK_PER_SM = 15.82  # profiles/r01/pipe_peaks.json (mufu_ex2)
 
 
 def _peaks():
@@ -529,6 +530,8 @@ def run_ours(args):
             "peak_source": f"{sms} SMs x {MUFU_PER_CLK_PER_SM} MUFU/clk x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
             "frac_at_run_clock": (achieved / (sms * MUFU_PER_CLK_PER_SM * clocks["sm_mhz"] * 1e6)
                                   if clocks.get("sm_mhz") else None),
+            # against the microbenchmarked MUFU rate (tools/pipe_peaks.cu: 15.82 ex2/clk/SM)
+            "frac_vs_measured_mufu": achieved / (sms * MUFU_MEASURED_PER_CLK_PER_SM * sm_max * 1e6),
             "kernel_ms": sc_ms, "fk_ms": fk_ms,
             "fk_hbm_GBps": Q * (wl.robot.dof * 4 + M * 16) / (fk_ms * 1e-3) * 1e-9,
             "fk_hbm_frac": Q * (wl.robot.dof * 4 + M * 16) / (fk_ms * 1e-3) * 1e-9 / float(peaks.get("hbm_gbs", 6554.6))}
