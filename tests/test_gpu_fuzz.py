@@ -82,3 +82,39 @@ def test_gram_and_edges_fuzz(seed):
     ref_hit, fmax = oracle.edge(robot, qa, qb, ni, kind, gamma, oracle.fk(robot, X), alpha)[:2]
     sure = np.abs(fmax) > 1e-4
     assert np.array_equal(hit.cpu().numpy()[sure], ref_hit[sure])
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_train_fuzz(seed):
+    """Algorithm 1 on random small problems: the GPU trace equals the oracle's on the same
+    fp32 Gram (P-exact), with random beta, S_max, iter_max and labels; the lazy mode
+    equals the full-Gram run."""
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    rng = np.random.default_rng(3000 + seed)
+    robot = _robot(rng)
+    if robot.n_cp > 16:  # the lazy mode takes n_cp <= 16
+        robot = W.make_robot("fuzz16", robot.dh, robot.cp_frame[:16], robot.cp_offset[:16], base=robot.base)
+    kind = int(rng.integers(0, 2))
+    gamma = float(np.exp(rng.uniform(np.log(0.5), np.log(20.0))))
+    D = robot.dh.shape[0]
+    n = int(rng.integers(1, 400))
+    X = rng.uniform(-np.pi, np.pi, size=(n, D)).astype(np.float32)
+    y = np.where(rng.random(n) < rng.uniform(0.2, 0.8), 1, -1).astype(np.int8)
+    beta = float(rng.uniform(1.0, 3.0))
+    iter_max = int(rng.integers(0, 3000))
+    s_max = int(rng.integers(1, n + 1)) if rng.random() < 0.3 else None
+    pos = fb.fastron_fk(robot, dev(X))
+    K = fb.fastron_gram(pos, kind, gamma)
+    out = fb.fastron_train(K, dev(y), beta, iter_max, s_max)
+    lazy = fb.fastron_train_lazy(pos, dev(y), kind, gamma, beta, iter_max, s_max, cache_cols=int(rng.integers(0, n + 1)))
+    torch.cuda.synchronize()
+    res = fb.train_result(out["result"])
+    r = oracle.train(K.cpu().numpy().astype(np.float64), y, beta, iter_max, s_max)
+    it = res["iterations"]
+    assert it == r["iterations"] and res["n_support"] == len(r["support"])
+    assert np.array_equal(out["trace"].cpu().numpy()[:it], r["trace"])
+    assert np.abs(out["alpha"].cpu().numpy() - r["alpha"]).max() <= 1e-9 * max(1.0, np.abs(r["alpha"]).max())
+    assert fb.train_result(lazy["result"]) == res
+    assert np.array_equal(lazy["alpha"].cpu().numpy(), out["alpha"].cpu().numpy())
