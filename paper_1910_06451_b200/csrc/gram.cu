@@ -1,13 +1,16 @@
 // gram.cu — K3, the FK-kernel Gram matrix K_ij = K_FK(X_i, X_j) (
 // Algorithm 1's "computeKernelMatrixColumn").
 //
-// Upper-triangular 128x128 tiles (bi <= bj), one CTA of 4 warps per tile:
+// Upper-triangular 128x128 tiles (bi <= bj). One CTA of 4 warps owns a column block bj
+// and T consecutive row tiles bi of it (T = 1 for shallow triangles, up to 4 for deep
+// ones, so the column prologue is paid once per T tiles):
 //  * COLUMN points live in registers: each lane holds CPL consecutive columns (2 at
 //    M <= 16, 1 above) as pre-scaled f32x2 control-point pairs (the packed records of
 //    the scoring kernel); a warp covers 32*CPL columns;
-//  * the tile's 128 ROW points arrive as two packed support tiles by one TMA bulk copy;
-//    each warp walks a contiguous row range; a row record is a warp-broadcast
-//    LDS.128 + LDS.64 shared by the lane's CPL columns;
+//  * each tile's 128 ROW points arrive as two packed support tiles by TMA bulk copies
+//    into a 2-stage ring (tile t+1 loads while tile t computes); each warp walks a
+//    contiguous row range; a row record is a warp-broadcast LDS.128 + LDS.64 shared by
+//    the lane's CPL columns;
 //  * the (bi, bj) block is stored straight from registers: for a fixed row each lane
 //    writes its CPL consecutive floats as one vector store (the warp covers 32*CPL
 //    consecutive floats). The lane keeps its last 4 rows x CPL values in registers and
@@ -41,15 +44,24 @@ constexpr int kGB = 128;             // tile edge (2 support tiles)
 #endif
 constexpr int kChunkRows = FASTRON_GRAM_CHUNK;  // rows per mirror chunk (held in registers): 4 or 8
 
-__device__ __forceinline__ void tile_coords(int64_t t, int64_t nb, int64_t& bi, int64_t& bj) {
-  // row-major enumeration of the upper triangle: row bi holds tiles bi..nb-1
-  double d = (double)(2 * nb + 1);
-  int64_t r = (int64_t)((d - sqrt(d * d - 8.0 * (double)t)) * 0.5);
-  auto start = [&](int64_t row) { return row * nb - row * (row - 1) / 2; };
-  while (r > 0 && start(r) > t) --r;
-  while (start(r + 1) <= t) ++r;
-  bi = r;
-  bj = r + (t - start(r));
+// Work units, column-block-major: column block b holds row tiles 0..b (the upper triangle),
+// cut into ceil((b+1)/T) units of T consecutive row tiles. units_before(b) = sum over
+// k = 1..b of ceil(k/T) = T*q*(q+1)/2 + r*(q+1) with b = q*T + r.
+__host__ __device__ inline int64_t units_before(int64_t b, int T) {
+  const int q = (int)b / T, r = (int)b - q * T;  // b < 2^31 (the launch checks units < 2^31)
+  return (int64_t)T * q * (q + 1) / 2 + (int64_t)r * (q + 1);
+}
+
+__device__ __forceinline__ void unit_coords(int64_t u, int64_t nb, int T, int64_t& bj, int64_t& bi_first) {
+  // largest b with units_before(b) <= u: units_before(b) ~ (b^2 + T*b) / (2T), so start
+  // from the root of b^2 + T*b - 2*T*u and step to the exact value (no 64-bit divisions)
+  const double t = (double)T;
+  int64_t b = (int64_t)((sqrt(t * t + 8.0 * t * (double)u) - t) * 0.5);
+  b = b < 0 ? 0 : b > nb - 1 ? nb - 1 : b;
+  while (b > 0 && units_before(b, T) > u) --b;
+  while (b + 1 < nb && units_before(b + 1, T) <= u) ++b;
+  bj = b;
+  bi_first = (u - units_before(b, T)) * T;
 }
 
 #ifndef FASTRON_GRAM_RI4
@@ -69,7 +81,7 @@ __host__ __device__ constexpr int gram_min_blocks(int mp) { return mp <= 8 ? 4 :
 template <int MP, int KIND, bool JOINT>
 __global__ void __launch_bounds__(kGT, gram_min_blocks(MP))
     gram_kernel(const float* __restrict__ packed, int64_t n, int M, int m_pow2, float inv_m, float* __restrict__ K,
-                int64_t ldk) {
+                int64_t ldk, int T) {
   constexpr int NP = MP / 2;
   constexpr int CPL = gram_cpl(MP);           // columns per lane
   constexpr int RI = CPL >= 4 ? FASTRON_GRAM_RI4 : FASTRON_GRAM_RI2;  // rows interleaved per pair loop
@@ -80,15 +92,21 @@ __global__ void __launch_bounds__(kGT, gram_min_blocks(MP))
   constexpr int64_t TF = tile_floats(MP);
   constexpr uint32_t TB = (uint32_t)tile_bytes(MP);
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
-  float* rows = reinterpret_cast<float*>(smem_raw + 128);  // 2 packed tiles
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);  // one mbarrier per row stage
+  float* const stage0 = reinterpret_cast<float*>(smem_raw + 128);  // stage s: 2 packed tiles at stage0 + 2*TF*s
 
+  // the CTA's unit: column block bj and its row tiles bi_first..bi_last (<= bj), T per unit
   const int64_t nb = (n + kGB - 1) / kGB;
-  int64_t bi, bj;
-  tile_coords(blockIdx.x, nb, bi, bj);
-  const int64_t i0 = bi * kGB, j0 = bj * kGB;
+  int64_t bj, bi_first;
+  unit_coords(blockIdx.x, nb, T, bj, bi_first);
+  const int64_t bi_last = min(bj, bi_first + T - 1);
+  const int64_t j0 = bj * kGB;
   const int64_t n_tiles = (n + kTileSupports - 1) / kTileSupports;
-  const int rt = (n_tiles - 2 * bi) >= 2 ? 2 : 1;  // row tiles present
+  auto issue_rows = [&](int64_t bi, int s) {  // TMA the row tile pair of block bi into stage s
+    const int rt = (n_tiles - 2 * bi) >= 2 ? 2 : 1;
+    mbar_expect_tx(bar + s, TB * rt);
+    for (int c = 0; c < rt; ++c) tma_bulk_g2s(stage0 + (2 * s + c) * TF, packed + (2 * bi + c) * TF, TB, bar + s);
+  };
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int cg = warp % G, rg = warp / G;
@@ -96,13 +114,11 @@ __global__ void __launch_bounds__(kGT, gram_min_blocks(MP))
   const int rbase = rg * RW;   // first row of this warp (tile-relative)
   if (tid == 0) {
     mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
     fence_barrier_init();
   }
   __syncthreads();
-  if (tid == 0) {
-    mbar_expect_tx(bar, TB * rt);
-    for (int c = 0; c < rt; ++c) tma_bulk_g2s(rows + c * TF, packed + (2 * bi + c) * TF, TB, bar);
-  }
+  if (tid == 0) issue_rows(bi_first, 0);
 
   // the lane's CPL consecutive columns cbase + CPL*lane + h, read from the packed (scaled) records
   f2 ux[CPL][NP], uy[CPL][NP], uz[CPL][NP];
@@ -128,14 +144,20 @@ __global__ void __launch_bounds__(kGT, gram_min_blocks(MP))
       uz[h][NP - 1] = pk(lo(uz[h][NP - 1]), 0.0f);
     }
   }
-  mbar_wait(bar, 0);
-
-  const bool mirror = bi != bj;
-  const int rows_here = (int)min((int64_t)kGB, n - i0);
   const int64_t c0 = j0 + cbase + CPL * lane;  // the lane's first column
   const bool cols_full = c0 + CPL <= n;
   // vector stores need CPL-float (direct) and 32-byte (mirror) alignment of the rows
   const bool vec_ok = (ldk % 8) == 0 && (reinterpret_cast<uintptr_t>(K) & 31) == 0;
+
+  // the unit's row tiles stream through a 2-stage TMA ring; the columns stay in registers
+  for (int64_t bi = bi_first; bi <= bi_last; ++bi) {
+  const int t = (int)(bi - bi_first), s = t & 1;
+  if (tid == 0 && bi < bi_last) issue_rows(bi + 1, s ^ 1);  // stage s^1 was released below
+  mbar_wait(bar + s, (t >> 1) & 1);
+  const float* rows = stage0 + 2 * s * TF;
+  const int64_t i0 = bi * kGB;
+  const bool mirror = bi != bj;
+  const int rows_here = (int)min((int64_t)kGB, n - i0);
   // fixed trip counts (no early exits) so loads of the next row overlap this row's math;
   // rows past the matrix edge are computed on stale shared memory but never stored
   const int q_end = min(RW, ((rows_here - rbase + kChunkRows - 1) / kChunkRows) * kChunkRows);
@@ -230,22 +252,47 @@ __global__ void __launch_bounds__(kGT, gram_min_blocks(MP))
       }
     }
   }
+  __syncthreads();  // every warp is done with stage s before it is refilled
+  }
+}
+
+// row tiles per CTA: 1 while the triangle is only a few waves deep (occupancy first);
+// for deep triangles up to 4, keeping >= ~4 waves of units so the tail stays short
+// (measured at N = 20,000, M = 16: T = 1, 2, 4, 6, 8 -> 1.11, 1.03, 1.01, 1.03, 1.05 ms).
+// Two row stages then cost 4 tiles of shared memory, which fits the resident CTAs for
+// MP <= 16 only. FASTRON_GRAM_T overrides (probing).
+static int gram_rows_per_unit(int64_t tiles, int mp) {
+  static const int env = [] {
+    const char* e = getenv("FASTRON_GRAM_T");
+    return e ? atoi(e) : 0;
+  }();
+  if (env > 0) return env;
+  if (mp > 16) return 1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t slots = (int64_t)sms * gram_min_blocks(mp);
+  int64_t T = tiles / (4 * slots);
+  return (int)(T < 1 ? 1 : T > 4 ? 4 : T);
 }
 
 template <int MP, int KIND, bool JOINT = false>
 static cudaError_t run_gram(const float* packed, int64_t n, int M, float* K, int64_t ldk, cudaStream_t st) {
-  const size_t smem = 128 + 2 * tile_bytes(MP);
+  const int64_t nb = (n + kGB - 1) / kGB;
+  const int64_t tiles = nb * (nb + 1) / 2;
+  const int T = gram_rows_per_unit(tiles, MP);
+  const size_t smem = 128 + (T > 1 ? 4 : 2) * tile_bytes(MP);  // one or two row stages
   static std::atomic<int> attr[kMaxDevices];
   const int dev = device_slot();
   if (!attr[dev].load()) {
-    cudaFuncSetAttribute(gram_kernel<MP, KIND, JOINT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(gram_kernel<MP, KIND, JOINT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(128 + 4 * tile_bytes(MP)));
     attr[dev].store(1);
   }
-  const int64_t nb = (n + kGB - 1) / kGB;
-  const int64_t tiles = nb * (nb + 1) / 2;
-  if (tiles > 0x7fffffff) return cudaErrorInvalidValue;
+  const int64_t units = units_before(nb, T);
+  if (units > 0x7fffffff) return cudaErrorInvalidValue;
   const int m_pow2 = (M & (M - 1)) == 0;
-  gram_kernel<MP, KIND, JOINT><<<(unsigned)tiles, kGT, smem, st>>>(packed, n, M, m_pow2, 1.0f / (float)M, K, ldk);
+  gram_kernel<MP, KIND, JOINT><<<(unsigned)units, kGT, smem, st>>>(packed, n, M, m_pow2, 1.0f / (float)M, K, ldk, T);
   g_launches.fetch_add(1);
   return cudaGetLastError();
 }

@@ -198,3 +198,45 @@ def test_train_cluster_path_trace_exact():
     g = _gpu_train(K, y, 1.0, 20_000)
     r = oracle.train(K.cpu().numpy().astype(np.float64), y, 1.0, 20_000)
     _assert_same_run(g, r)
+
+
+_GRAM_T_CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_1910_06451_b200 as fb, workloads as W
+out = []
+for M, n, kind in ((16, 1000, 0), (5, 777, 1), (8, 1, 0), (8, 129, 0)):
+    rng = np.random.default_rng(M + n)
+    base = W.arm7(8)
+    robot = W.make_robot("t%d" % M, base.dh, rng.integers(0, 8, size=M), rng.uniform(-0.1, 0.1, size=(M, 3)))
+    X = rng.uniform(-np.pi, np.pi, size=(n, 7)).astype(np.float32)
+    pos = fb.fastron_fk(robot, torch.from_numpy(X).cuda())
+    K = torch.full((n, n + 8), -7.0, device="cuda")
+    fb.fastron_gram(pos, kind, 5.0, K=K[:, :n])
+    torch.cuda.synchronize()
+    out.append(K.cpu().numpy())
+np.savez({path!r}, *out)
+"""
+
+
+@pytest.mark.parametrize("T", [2, 3, 4])
+def test_gram_row_streaming_units_bit_identical(T, tmp_path):
+    """K3 streams T row tiles per CTA through a 2-stage TMA ring (T = 4 at the cfg5 size,
+    1 at small N). Forcing T (FASTRON_GRAM_T, read once per process) in a child process must
+    give the T = 1 matrix bit for bit — partial units, ragged last tiles, odd M, ldk > n."""
+    require_gpu()
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = _GRAM_T_CHILD.format(root=root, path=str(tmp_path / "k.npz"))
+    env = dict(os.environ, FASTRON_GRAM_T="1")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env)
+    ref = np.load(tmp_path / "k.npz")
+    ref = [ref["arr_%d" % i] for i in range(len(ref.files))]
+    env["FASTRON_GRAM_T"] = str(T)
+    subprocess.run([sys.executable, "-c", code], check=True, env=env)
+    got = np.load(tmp_path / "k.npz")
+    for i, r in enumerate(ref):
+        g = got["arr_%d" % i]
+        assert np.array_equal(g, r), (T, i)
+        assert np.all(g[:, r.shape[0]:] == -7.0)
