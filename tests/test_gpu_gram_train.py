@@ -211,8 +211,8 @@ for M, n, kind in ((16, 1000, 0), (5, 777, 1), (8, 1, 0), (8, 129, 0)):
     robot = W.make_robot("t%d" % M, base.dh, rng.integers(0, 8, size=M), rng.uniform(-0.1, 0.1, size=(M, 3)))
     X = rng.uniform(-np.pi, np.pi, size=(n, 7)).astype(np.float32)
     pos = fb.fastron_fk(robot, torch.from_numpy(X).cuda())
-    K = torch.full((n, n + 8), -7.0, device="cuda")
-    fb.fastron_gram(pos, kind, 5.0, K=K[:, :n])
+    K = torch.full((n + 2, n + 8), -7.0, device="cuda")  # guard rows and columns
+    fb.fastron_gram(pos, kind, 5.0, K=K[:n, :n])
     torch.cuda.synchronize()
     out.append(K.cpu().numpy())
 np.savez({path!r}, *out)
@@ -238,5 +238,7 @@ def test_gram_row_streaming_units_bit_identical(T, tmp_path):
     got = np.load(tmp_path / "k.npz")
     for i, r in enumerate(ref):
         g = got["arr_%d" % i]
+        n = r.shape[0] - 2
         assert np.array_equal(g, r), (T, i)
-        assert np.all(g[:, r.shape[0]:] == -7.0)
+        assert np.all(g[:, n:] == -7.0) and np.all(g[n:, :] == -7.0)
+        assert np.all(np.diag(g[:n, :n]) == 1.0) and np.array_equal(g[:n, :n], g[:n, :n].T)
