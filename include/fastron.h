@@ -165,7 +165,7 @@ fastron_status fastron_gram(const float* pos, int64_t n, int64_t ldp, int32_t n_
 /*
  * fastron_train — Algorithm 1, "Fastron Model Update Algorithm" (PAPER.md:206-252,
  * Eq. 6-9), run entirely on the device in one persistent cluster kernel (one CTA up to
- * 6,144 points; above, a cluster of ~n/1024 CTAs up to 16, chosen by the library).
+ * 2,048 points; above, a cluster of ~n/1024 CTAs up to 16, chosen by the library).
  *   K: device float [n][ldk] Gram (from fastron_gram; promoted to fp64 on read).
  *   y: device int8 [n], +1 = C_obs, -1 = C_free.
  *   beta >= 1: conditional bias, b_i = beta^(0.5 (y_i + 1)).

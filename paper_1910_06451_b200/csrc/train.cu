@@ -1,8 +1,8 @@
 // train.cu — K5, Algorithm 1 "Fastron Model Update Algorithm" (PAPER.md:206-252,
 // Eq. 6-9) as ONE persistent kernel: no host round trip per iteration.
 //
-// A thread-block cluster of C CTAs (C = 1..16, 512 threads each) owns the training
-// state on chip. Thread t of CTA r owns the EPT slots j = k*512 + t (k < EPT) of the
+// A thread-block cluster of C CTAs (C = 1..16, 256 threads each) owns the training
+// state on chip. Thread t of CTA r owns the EPT slots j = k*256 + t (k < EPT) of the
 // CTA's slice [r*chunk, r*chunk + len). The margins are kept signed by the label,
 // G = y F, in registers; Y = y alpha (>= 0 by the constraint
 // y_i alpha_i >= 0) lives in shared memory and is only touched by its
@@ -40,10 +40,13 @@ namespace cg = cooperative_groups;
 
 namespace fastron {
 
-constexpr int kTrainNT = 512;
+#ifndef FASTRON_TRAIN_NT
+#define FASTRON_TRAIN_NT 256
+#endif
+constexpr int kTrainNT = FASTRON_TRAIN_NT;
 constexpr int kTrainWarps = kTrainNT / 32;
 constexpr int kMaxCluster = 16;
-constexpr int kMaxEPT = 12;                                 // slots per thread in registers
+constexpr int kMaxEPT = 6144 / kTrainNT;                    // slots per thread in registers
 constexpr int64_t kChunkMax = (int64_t)kTrainNT * kMaxEPT;  // 6144 slots per CTA
 constexpr int kNone = 0x7fffffff;
 
@@ -654,6 +657,29 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
 
 int64_t train_max_n() { return kChunkMax * kMaxCluster; }
 
+// Cluster size for n points when a CTA holds at most chunk_max. Up to 2,048 points one
+// CTA (8 slots per thread) beats any cluster, whose winner exchange costs ~0.15 us per
+// iteration; above, ~1,024 points per CTA (4 slots per thread) — measured at 256 threads
+// (tools/train_sweep.py, us / iteration): N = 2,000 C = 1 0.98, C = 2 1.14; N = 3,000
+// C = 1 1.16, C = 3 1.14; N = 5,000 C = 1 1.50, C = 4 1.31 (8 slots), C = 5 1.15,
+// C = 8 1.16; N = 8,446 C = 9 1.30, C = 12 1.31. FASTRON_TRAIN_CLUSTER sets C (tuning and
+// tests; never below the minimum that fits).
+static int train_cluster_size(int64_t n, int64_t chunk_max) {
+  int64_t C = (n + chunk_max - 1) / chunk_max;  // the minimum that fits
+  if (C < 1) C = 1;
+  const int64_t c_min = C;
+  if (n > 2048) {
+    int64_t c_small = (n + 1023) / 1024;
+    if (c_small > kMaxCluster) c_small = kMaxCluster;
+    if (c_small > C) C = c_small;
+  }
+  if (const char* env = getenv("FASTRON_TRAIN_CLUSTER")) {
+    const int64_t c = atoi(env);
+    C = c > c_min ? c : c_min;
+  }
+  return (int)C;
+}
+
 template <int EPT, int LMP = 0, int LKIND = 0>
 static cudaError_t launch_ept(const TrainArgs& A, int C, cudaStream_t st, size_t smem) {
   static std::atomic<int> attr[kMaxDevices];
@@ -681,19 +707,7 @@ static cudaError_t launch_ept(const TrainArgs& A, int C, cudaStream_t st, size_t
 cudaError_t launch_train(const float* K, int64_t n, int64_t ldk, const int8_t* y, double beta, int64_t iter_max,
                          int64_t s_max, double* alpha, double* F, int32_t* support_idx, int32_t* trace, void* result,
                          cudaStream_t st) {
-  int C = (int)((n + kChunkMax - 1) / kChunkMax);
-  if (C < 1) C = 1;
-  // Above one CTA the winner exchange is paid anyway, and smaller slices shorten the scan:
-  // ~1,024 points per CTA (tools/train_big_probe.py: N = 8,446 C = 2 1.76, 4 1.59, 9 1.43,
-  // 16 1.46 us / iteration; N = 20,000 C = 4 2.00, 8 1.83, 12 1.76, 16 1.77).
-  if (C > 1) {
-    const int c_small = (int)((n + 1023) / 1024);
-    C = c_small > C ? (c_small < kMaxCluster ? c_small : kMaxCluster) : C;
-  }
-  if (const char* env = getenv("FASTRON_TRAIN_CLUSTER")) {  // tuning override (>= the minimum)
-    const int c = atoi(env);
-    if (c > C) C = c;
-  }
+  const int C = train_cluster_size(n, kChunkMax);
   if (C > kMaxCluster) return cudaErrorInvalidValue;
   TrainArgs A;
   A.K = K;
@@ -720,25 +734,28 @@ cudaError_t launch_train(const float* K, int64_t n, int64_t ldk, const int8_t* y
   const size_t smem = (size_t)A.chunk * 8;
   cudaError_t e;
   // the smallest instance that covers the slice: dead slots still cost a load and an update
-  if (ept <= 2) e = launch_ept<2>(A, C, st, smem);
-  else if (ept <= 4) e = launch_ept<4>(A, C, st, smem);
-  else if (ept <= 6) e = launch_ept<6>(A, C, st, smem);
-  else if (ept <= 8) e = launch_ept<8>(A, C, st, smem);
-  else if (ept <= 10) e = launch_ept<10>(A, C, st, smem);
-  else e = launch_ept<12>(A, C, st, smem);
+  // instances at sixths of the register budget (4, 8, ..., 24 slots at 256 threads)
+  constexpr int E = kMaxEPT / 6;
+  if (ept <= E) e = launch_ept<E>(A, C, st, smem);
+  else if (ept <= 2 * E) e = launch_ept<2 * E>(A, C, st, smem);
+  else if (ept <= 3 * E) e = launch_ept<3 * E>(A, C, st, smem);
+  else if (ept <= 4 * E) e = launch_ept<4 * E>(A, C, st, smem);
+  else if (ept <= 5 * E) e = launch_ept<5 * E>(A, C, st, smem);
+  else e = launch_ept<6 * E>(A, C, st, smem);
   g_launches.fetch_add(1);
   return e;
 }
 
 // ---- lazy-column mode ----
 constexpr int64_t kLazySmem = 200 * 1024;  // shared-memory budget per CTA
+constexpr int kLazyMaxEPT = 8;             // slots per thread in the lazy mode
 
 static int64_t lazy_bytes_per_slot(int MP) { return 8 + 4 + (int64_t)(MP / 2) * 24; }
 
 int64_t train_lazy_max_n(int M) {
   const int MP = padded_m(M);
   int64_t chunk = kLazySmem / lazy_bytes_per_slot(MP);
-  if (chunk > 4 * kTrainNT) chunk = 4 * kTrainNT;
+  if (chunk > kLazyMaxEPT * kTrainNT) chunk = kLazyMaxEPT * kTrainNT;
   return chunk * kMaxCluster;
 }
 
@@ -746,7 +763,8 @@ template <int MP, int KIND>
 static cudaError_t launch_lazy_mp(const TrainArgs& A, int C, cudaStream_t st, size_t smem) {
   const int64_t ept = (A.chunk + kTrainNT - 1) / kTrainNT;
   if (ept <= 2) return launch_ept<2, MP, KIND>(A, C, st, smem);
-  return launch_ept<4, MP, KIND>(A, C, st, smem);
+  if (ept <= 4) return launch_ept<4, MP, KIND>(A, C, st, smem);
+  return launch_ept<kLazyMaxEPT, MP, KIND>(A, C, st, smem);
 }
 
 cudaError_t launch_train_lazy(const float* packed, int64_t n, int M, int kind, const int8_t* y, double beta,
@@ -754,17 +772,8 @@ cudaError_t launch_train_lazy(const float* packed, int64_t n, int M, int kind, c
                               int32_t* trace, void* result, float* cache, int64_t cache_cols, cudaStream_t st) {
   const int MP = padded_m(M);
   int64_t chunk_max = kLazySmem / lazy_bytes_per_slot(MP);
-  if (chunk_max > 4 * kTrainNT) chunk_max = 4 * kTrainNT;
-  int C = (int)((n + chunk_max - 1) / chunk_max);
-  if (C < 1) C = 1;
-  if (C > 1) {  // as in launch_train: ~1,024 points per CTA once the exchange is paid
-    const int c_small = (int)((n + 1023) / 1024);  // (lazy cfg3: C = 3 1.62, 5 1.43, 8 1.46 us)
-    C = c_small > C ? (c_small < kMaxCluster ? c_small : kMaxCluster) : C;
-  }
-  if (const char* env = getenv("FASTRON_TRAIN_CLUSTER")) {
-    const int c = atoi(env);
-    if (c > C) C = c;
-  }
+  if (chunk_max > kLazyMaxEPT * kTrainNT) chunk_max = kLazyMaxEPT * kTrainNT;
+  const int C = train_cluster_size(n, chunk_max);  // as in launch_train (lazy cfg3: C = 5)
   if (C > kMaxCluster) return cudaErrorInvalidValue;
   TrainArgs A;
   A.K = nullptr;

@@ -187,9 +187,9 @@ def test_cfg5_gram_full_size_sampled_rows():
 
 
 def test_train_cluster_path_trace_exact():
-    """n = 6,145 > one CTA's 6,144 register slots: Algorithm 1 runs on a 2-CTA cluster
-    (slices of 3,073 and 3,072, DSMEM candidate exchange); the trace, alpha and F must still
-    equal the oracle's on the same Gram."""
+    """n = 6,145 > one CTA's 6,144 register slots: Algorithm 1 runs on a 7-CTA cluster
+    (slices of 878, DSMEM candidate exchange); the trace, alpha and F must still equal the
+    oracle's on the same Gram."""
     require_gpu()
     robot, X = W.arm7(8), W.cfg5_gram_workload(6145)[1]
     cubes = W.train_workload().cubes
@@ -242,3 +242,25 @@ def test_gram_row_streaming_units_bit_identical(T, tmp_path):
         assert np.array_equal(g, r), (T, i)
         assert np.all(g[:, n:] == -7.0) and np.all(g[n:, :] == -7.0)
         assert np.all(np.diag(g[:n, :n]) == 1.0) and np.array_equal(g[:n, :n], g[:n, :n].T)
+
+
+def test_train_every_cluster_size_same_run():
+    """The training state can be split over any cluster size; C only changes the slices,
+    the slot instances (C = 1 puts 20 slots in each of 256 threads: the largest register
+    instances, otherwise used only above 32k points) and the exchange — never the run.
+    cfg3 (N = 5,000) at C = 1, 2, 3, 5 (default), 16 against the oracle's trace."""
+    require_gpu()
+    wl = W.train_workload()
+    y = _labels(wl)
+    _, K = _gram(wl.robot, wl.X, 0, wl.gamma)
+    r = oracle.train(K.cpu().numpy().astype(np.float64), y, 1.0, wl.iter_max)
+    old = os.environ.get("FASTRON_TRAIN_CLUSTER")
+    try:
+        for C in (1, 2, 3, 5, 16):
+            os.environ["FASTRON_TRAIN_CLUSTER"] = str(C)
+            _assert_same_run(_gpu_train(K, y, 1.0, wl.iter_max), r)
+    finally:
+        if old is None:
+            os.environ.pop("FASTRON_TRAIN_CLUSTER", None)
+        else:
+            os.environ["FASTRON_TRAIN_CLUSTER"] = old

@@ -1,4 +1,4 @@
-"""Algorithm 1 at N > 6,144 (the cluster path) for several cluster sizes: the update
+"""Algorithm 1 at N > 2,048 (the cluster path) for several cluster sizes: the update
 cycle's 8,446-point set size and 20,000. Traces must agree across C."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
