@@ -70,4 +70,52 @@ __device__ __forceinline__ void fk_chain(const FkParams& P, QFun q, Emit emit) {
   }
 }
 
+// The same chain for NC configurations per thread: the per-joint parameters and the
+// frame table are read once for all NC, and the NC chains give the scheduler independent
+// fp64 work. Each configuration's arithmetic is fk_chain's, expression for expression,
+// so its positions are the same bits. q(c, j): joint j of configuration c;
+// emit(c, m, x, y, z).
+template <int NC, class QFun, class Emit>
+__device__ __forceinline__ void fk_chain_multi(const FkParams& P, QFun q, Emit emit) {
+  double c0x[NC], c0y[NC], c0z[NC], c1x[NC], c1y[NC], c1z[NC], c2x[NC], c2y[NC], c2z[NC], px[NC], py[NC], pz[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    c0x[c] = P.base_c[0][0]; c0y[c] = P.base_c[0][1]; c0z[c] = P.base_c[0][2];
+    c1x[c] = P.base_c[1][0]; c1y[c] = P.base_c[1][1]; c1z[c] = P.base_c[1][2];
+    c2x[c] = P.base_c[2][0]; c2y[c] = P.base_c[2][1]; c2z[c] = P.base_c[2][2];
+    px[c] = P.base_p[0]; py[c] = P.base_p[1]; pz[c] = P.base_p[2];
+  }
+  auto emit_frame = [&](int j) {
+    for (int idx = P.frame_begin[j]; idx < P.frame_begin[j + 1]; ++idx) {
+      const int m = P.frame_list[idx];
+      const double tx = P.cp_off[m][0], ty = P.cp_off[m][1], tz = P.cp_off[m][2];
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        emit(c, m, px[c] + c0x[c] * tx + c1x[c] * ty + c2x[c] * tz, py[c] + c0y[c] * tx + c1y[c] * ty + c2y[c] * tz,
+             pz[c] + c0z[c] * tx + c1z[c] * ty + c2z[c] * tz);
+    }
+  };
+  emit_frame(0);
+#pragma unroll 1
+  for (int j = 0; j < P.dof; ++j) {
+    const double ca = P.ca[j], sa = P.sa[j], a = P.a[j], d = P.d[j], off = P.theta_off[j];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      double s, c;
+      sincos(q(k, j) + off, &s, &c);
+      const double n0x = c * c0x[k] + s * c1x[k], n0y = c * c0y[k] + s * c1y[k], n0z = c * c0z[k] + s * c1z[k];
+      const double vx = c * c1x[k] - s * c0x[k], vy = c * c1y[k] - s * c0y[k], vz = c * c1z[k] - s * c0z[k];
+      px[k] += a * n0x + d * c2x[k];
+      py[k] += a * n0y + d * c2y[k];
+      pz[k] += a * n0z + d * c2z[k];
+      const double n1x = ca * vx + sa * c2x[k], n1y = ca * vy + sa * c2y[k], n1z = ca * vz + sa * c2z[k];
+      const double n2x = ca * c2x[k] - sa * vx, n2y = ca * c2y[k] - sa * vy, n2z = ca * c2z[k] - sa * vz;
+      c0x[k] = n0x; c0y[k] = n0y; c0z[k] = n0z;
+      c1x[k] = n1x; c1y[k] = n1y; c1z[k] = n1z;
+      c2x[k] = n2x; c2y[k] = n2y; c2z[k] = n2z;
+    }
+    emit_frame(j + 1);
+  }
+}
+
 }  // namespace fastron

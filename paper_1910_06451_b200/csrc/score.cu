@@ -45,7 +45,22 @@ constexpr int kSupUnroll = FASTRON_SUP_UNROLL;  // supports per unrolled step of
 constexpr int kNT = FASTRON_SCORE_NT;  // threads per scoring CTA
 constexpr int kStages = FASTRON_SCORE_STAGES;  // TMA ring depth
 
-__host__ __device__ constexpr int qt_for(int mp) { return mp <= 4 ? 8 : mp <= 8 ? 4 : mp <= 16 ? 2 : 1; }
+#ifndef FASTRON_QT4
+#define FASTRON_QT4 4
+#endif
+#ifndef FASTRON_QT8
+#define FASTRON_QT8 3
+#endif
+#ifndef FASTRON_QT16
+#define FASTRON_QT16 3
+#endif
+// queries per thread (A/B on the B200, bit-identical scores): M = 8: QT = 3
+// (122 registers, 4 resident CTAs) beats 4 (158, 3 CTAs) by 1.2 % on the headline, 2/5/6
+// are slower; M = 16: 3 (244 registers, 2 CTAs) beats 2 by 2 % and 1 by 15 %; M = 4:
+// 4 (94 registers, 5 CTAs) beats 8 by 3.5 %.
+__host__ __device__ constexpr int qt_for(int mp) {
+  return mp <= 4 ? FASTRON_QT4 : mp <= 8 ? FASTRON_QT8 : mp <= 16 ? FASTRON_QT16 : 1;
+}
 
 int padded_m(int M) { return (M + 1) & ~1; }
 int64_t n_support_tiles(int64_t ns) { return (ns + kTileSupports - 1) / kTileSupports; }

@@ -18,6 +18,12 @@ e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=Tr
 e0.record(); [step() for _ in range(5)]; e1.record(); e1.synchronize()
 ms = e0.elapsed_time(e1) / 5
 s = sc.cpu().numpy().astype(np.float64)
+if os.environ.get("NO_ORACLE"):  # timing + output hash only (A/B of bit-identical variants)
+    import hashlib
+    print(json.dumps({"lib": os.environ.get("FASTRON_LIB", "default"), "kind": wl.kind, "ms": ms,
+                      "frac": 1e6 * 2e4 * 8 / (ms * 1e-3) / (148 * 16 * 1.965e9),
+                      "sha": hashlib.sha1(sc.cpu().numpy().tobytes()).hexdigest()[:12]}), flush=True)
+    sys.exit(0)
 rng = np.random.default_rng(1)
 idx = np.unique(np.concatenate([rng.choice(len(s), 3000, replace=False), np.argsort(np.abs(s))[:1000]]))
 f, _ = oracle.score(wl.kind, wl.gamma, oracle.fk(wl.robot, wl.queries[idx]), oracle.fk(wl.robot, wl.supports), wl.alpha)

@@ -1,6 +1,6 @@
 """Time fastron_fk (K1) on the headline batch (1M x 7 joints, M = 8) and cfg5's M = 16;
 one JSON line (FASTRON_LIB selects the library build)."""
-import json, os, sys
+import hashlib, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_1910_06451_b200 as fb, workloads as W
@@ -20,5 +20,6 @@ for name, n_cp in (("m8", 8), ("m16", 16)):
         ts.append(e0.elapsed_time(e1))
     ms = float(np.median(ts))
     byts = len(q) * (4 * 7 + 16 * n_cp)
-    out[name] = {"us": ms * 1e3, "GBps": byts / ms * 1e-6, "hbm_frac": byts / ms * 1e-6 / 6554.6}
+    out[name] = {"us": ms * 1e3, "GBps": byts / ms * 1e-6, "hbm_frac": byts / ms * 1e-6 / 6554.6,
+                 "sha": hashlib.sha1(pos.cpu().numpy().tobytes()).hexdigest()[:12]}
 print(json.dumps(out), flush=True)

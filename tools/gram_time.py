@@ -1,5 +1,5 @@
 """Time fastron_gram on cfg3 (N=5000, M=8) and a 20k M=16 case (cfg5 size); one JSON line."""
-import json, os, sys
+import hashlib, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1910_06451_b200 as fb, workloads as W
@@ -21,5 +21,6 @@ for name, (robot, X) in {"cfg3": (W.train_workload().robot, W.train_workload().X
     ms = e0.elapsed_time(e1) / reps
     nb = (n + 127) // 128
     mufu = nb * (nb + 1) // 2 * 128 * 128 * robot.n_cp
-    out[name] = {"ms": ms, "mufu_frac": mufu / (ms * 1e-3) / (148 * 16 * 1.965e9), "write_GBps": n * n * 4 / ms * 1e-6}
+    out[name] = {"ms": ms, "mufu_frac": mufu / (ms * 1e-3) / (148 * 16 * 1.965e9), "write_GBps": n * n * 4 / ms * 1e-6,
+                 "sha": hashlib.sha1(K.cpu().numpy().tobytes()).hexdigest()[:12]}
 print(json.dumps(out), flush=True)
