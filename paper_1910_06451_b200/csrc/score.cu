@@ -414,6 +414,42 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ S
   }
 }
 
+// The same for many splits (> kSeqSplits): a CTA of 8 warps owns 32 consecutive queries;
+// warp w adds the w-th contiguous eighth of the splits in order, then warp 0 adds the 8
+// group sums in order — a fixed order (deterministic), 8x shorter dependency chains and
+// 8x more CTAs than the sequential kernel, which left a 4,096-query batch against 20k
+// supports (313 splits) 38 us in its finalize.
+constexpr int kSeqSplits = 16;
+template <int MODE>
+__global__ void __launch_bounds__(256) finalize_grouped_kernel(const __grid_constant__ ScoreArgs A) {
+  __shared__ double part[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t vq = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t nq_live = MODE == MODE_EDGE ? edge_active_queries(A) : A.nq;
+  if (MODE == MODE_EDGE && (int64_t)blockIdx.x * 32 >= nq_live) return;  // CTA-uniform
+  const int per = (A.n_splits + 7) / 8;
+  const int s0 = w * per, s1 = min(A.n_splits, s0 + per);
+  double f = 0.0;
+  if (vq < nq_live)
+    for (int sp = s0; sp < s1; ++sp) f += A.partial[(int64_t)sp * A.nq + vq];
+  part[w][lane] = f;
+  __syncthreads();
+  if (w != 0) return;
+  f = part[0][lane];
+#pragma unroll
+  for (int g = 1; g < 8; ++g) f += part[g][lane];
+  const double fm = f / A.denom;
+  if (MODE == MODE_POS || MODE == MODE_JOINT) {
+    if (vq < A.nq) {
+      if (A.score64) A.score64[vq] = fm;
+      if (A.score) A.score[vq] = (float)fm;
+      if (A.label) A.label[vq] = fm > 0.0 ? 1 : -1;
+    }
+  } else {
+    edge_vote(A, vq, fm);
+  }
+}
+
 // ---------------------------------------------------------------------------------
 // small batches (nq <= kSmallQ): support-parallel scoring
 // ---------------------------------------------------------------------------------
@@ -637,8 +673,12 @@ static cudaError_t run_score(const ScoreArgs& base, const FkParams& P, int64_t n
   g_launches.fetch_add(1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || plan.n_splits == 1) return e;
-  const int64_t fgrid = (nq + 255) / 256;
-  finalize_kernel<MODE><<<(unsigned)fgrid, 256, 0, st>>>(A);
+  if (plan.n_splits > kSeqSplits) {
+    finalize_grouped_kernel<MODE><<<(unsigned)((nq + 31) / 32), 256, 0, st>>>(A);
+  } else {
+    const int64_t fgrid = (nq + 255) / 256;
+    finalize_kernel<MODE><<<(unsigned)fgrid, 256, 0, st>>>(A);
+  }
   g_launches.fetch_add(1);
   return cudaGetLastError();
 }

@@ -38,7 +38,7 @@ def test_fk_parity_configs(name):
     _check(wl.robot, wl.supports)
 
 
-@pytest.mark.parametrize("n", [1, 31, 127, 129, 255, 257, 383, 1000])
+@pytest.mark.parametrize("n", [1, 31, 127, 129, 255, 257, 383, 1000, 65537, 65791])
 def test_fk_ragged_sizes_and_invariants(n):
     require_gpu()
     robot = W.arm7(16)
