@@ -219,12 +219,15 @@ __global__ void __launch_bounds__(256) edge_fk_kernel(const __grid_constant__ Sc
       });
 }
 
-template <int MP, int KIND, int MODE>
-// (no min-blocks argument: with one, ptxas allocates 182+ registers and only 2 CTAs fit
-// per SM — 4 % slower; without, 158 registers and 3 CTAs)
+// QTO > 0 overrides the queries per thread: batches of at most kNT queries use QT = 1 so
+// that a CTA does not evaluate 2 x kNT dead query slots (the summation order per query,
+// hence every bit, is the same for any QT)
+template <int MP, int KIND, int MODE, int QTO = 0>
+// (no min-blocks argument: with one, ptxas allocates more registers and fewer CTAs fit
+// per SM — measured slower)
 __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ ScoreArgs A,
                                                     const __grid_constant__ FkParams P) {
-  constexpr int QT = qt_for(MP);
+  constexpr int QT = QTO > 0 ? QTO : qt_for(MP);
   constexpr int NP = MP / 2;
   constexpr int64_t TF = tile_floats(MP);
   constexpr uint32_t TB = (uint32_t)tile_bytes(MP);
@@ -667,9 +670,21 @@ static cudaError_t run_score(const ScoreArgs& base, const FkParams& P, int64_t n
   A.n_splits = plan.n_splits;
   A.tiles_per_split = plan.tiles_per_split;
   const size_t smem = 128 + kStages * tile_bytes(MP);
+  const bool one_q = MODE != MODE_EDGE && nq <= kNT && qt_for(MP) > 1;  // one query per thread
+  if (one_q) plan.n_qblocks = (nq + kNT - 1) / kNT;
   const int64_t grid = plan.n_qblocks * plan.n_splits;
   if (grid > 0x7fffffff) return cudaErrorInvalidValue;
-  score_kernel<MP, KIND, MODE><<<(unsigned)grid, kNT, smem, st>>>(A, P);
+  if (one_q) {
+    static std::atomic<int> attr[kMaxDevices];
+    const int dev = device_slot();
+    if (!attr[dev].load()) {
+      cudaFuncSetAttribute(score_kernel<MP, KIND, MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr[dev].store(1);
+    }
+    score_kernel<MP, KIND, MODE, 1><<<(unsigned)grid, kNT, smem, st>>>(A, P);
+  } else {
+    score_kernel<MP, KIND, MODE><<<(unsigned)grid, kNT, smem, st>>>(A, P);
+  }
   g_launches.fetch_add(1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || plan.n_splits == 1) return e;
