@@ -76,7 +76,7 @@ __host__ __device__ constexpr int gram_cpl(int mp) {  // columns per lane
 }
 
 // resident CTAs per SM the register allocation must allow: 4 at M <= 8, 3 above
-__host__ __device__ constexpr int gram_min_blocks(int mp) { return mp <= 8 ? 4 : 3; }
+__host__ __device__ constexpr int gram_min_blocks(int mp) { return (mp <= 8 ? 16 : 12) / kGW; }
 
 template <int MP, int KIND, bool JOINT>
 __global__ void __launch_bounds__(kGT, gram_min_blocks(MP))
