@@ -250,3 +250,15 @@ def test_small_batches(M, kind):
     fb.fastron_query(robot, dev(q[:7]), spos, dev(alpha), kind, 5.0, score=sd, label=ld)
     torch.cuda.synchronize()
     assert np.array_equal(s1.cpu().numpy(), sd.cpu().numpy())
+
+
+@pytest.mark.parametrize("name,nq", [("headline", 33), ("headline", 100), ("headline", 128), ("headline", 129),
+                                     ("headline", 4096), ("cfg5", 64), ("cfg5", 1000)])
+def test_mid_batches_many_splits(name, nq):
+    """Batches between the small-batch kernel and the bulk path against 20k supports:
+    one query per thread (33..128 queries) and the grouped finalize (> 16 splits)."""
+    require_gpu()
+    wl = W.score_workload(name, n_queries=nq)
+    s, l = _gpu_scores(wl.robot, wl.supports, wl.alpha, wl.queries, 0, wl.gamma)
+    f, _ = _ref_scores(wl.robot, wl.supports, wl.alpha, wl.queries, 0, wl.gamma)
+    assert_score_parity(s, f, l, what=f"{name} nq={nq}")
