@@ -27,6 +27,23 @@ def test_joint_score_parity(kind, dof):
     assert_score_parity(sc.cpu().numpy(), f, lb.cpu().numpy(), what=f"joint kind={kind} dof={dof}")
 
 
+@pytest.mark.parametrize("nq", [33, 77, 128, 129])
+def test_joint_score_mid_batches(nq):
+    """33..128 queries take the one-query-per-thread instance; 20k supports give > 16
+    splits, so the grouped finalize sums them."""
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    rng = np.random.default_rng(nq)
+    s = rng.uniform(-np.pi, np.pi, size=(20_000, 7)).astype(np.float32)
+    a = rng.standard_normal(20_000).astype(np.float32)
+    q = rng.uniform(-np.pi, np.pi, size=(nq, 7)).astype(np.float32)
+    sc, lb = fb.fastron_score_joint(dev(q), dev(s), dev(a), 1, 0.1)
+    torch.cuda.synchronize()
+    f, _ = oracle.score_joint(1, 0.1, q, s, a)
+    assert_score_parity(sc.cpu().numpy(), f, lb.cpu().numpy(), what=f"joint nq={nq}")
+
+
 def test_joint_gram_parity_and_train():
     require_gpu()
     import torch
