@@ -101,5 +101,6 @@ int main() {
   run<true, true, 8>("packed f64acc QT=8", g, out);
   run<false, true, 8>("scalar f64acc QT=8", g, out);
   run<true, true, 6>("packed f64acc QT=6", g, out);
+  run<true, true, 3>("packed f64acc QT=3", g, out);
   return 0;
 }
