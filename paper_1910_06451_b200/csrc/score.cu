@@ -219,9 +219,9 @@ __global__ void __launch_bounds__(256) edge_fk_kernel(const __grid_constant__ Sc
       });
 }
 
-// QTO > 0 overrides the queries per thread: batches of at most kNT queries use QT = 1 so
-// that a CTA does not evaluate 2 x kNT dead query slots (the summation order per query,
-// hence every bit, is the same for any QT)
+// QTO > 0 overrides the queries per thread: small and mid-size batches use QT = 1 (more,
+// shorter CTAs and no dead query slots; the summation order per query, hence every bit,
+// is the same for any QT)
 template <int MP, int KIND, int MODE, int QTO = 0>
 // (no min-blocks argument: with one, ptxas allocates more registers and fewer CTAs fit
 // per SM — measured slower)
@@ -670,7 +670,11 @@ static cudaError_t run_score(const ScoreArgs& base, const FkParams& P, int64_t n
   A.n_splits = plan.n_splits;
   A.tiles_per_split = plan.tiles_per_split;
   const size_t smem = 128 + kStages * tile_bytes(MP);
-  const bool one_q = MODE != MODE_EDGE && nq <= kNT && qt_for(MP) > 1;  // one query per thread
+  // one query per thread up to a batch size measured per M (A/B, 20k supports, same bits):
+  // M = 8 up to 2,048 queries (512: 58 -> 46 us, 1,024: 73 -> 68, 2,048: 118 -> 113; 4,096
+  // slower), M = 16 up to 512 (256: 66 -> 58 us, 512: 97 -> 82; 1,024 slower)
+  const int64_t oneq_max = MP <= 4 ? kNT : MP <= 8 ? 2048 : 512;
+  const bool one_q = MODE != MODE_EDGE && nq <= oneq_max && qt_for(MP) > 1;
   if (one_q) plan.n_qblocks = (nq + kNT - 1) / kNT;
   const int64_t grid = plan.n_qblocks * plan.n_splits;
   if (grid > 0x7fffffff) return cudaErrorInvalidValue;
