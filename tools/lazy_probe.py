@@ -1,5 +1,7 @@
+"""Time fastron_train_lazy (Algorithm 1 with K columns computed on demand) on cfg3 for the
+cluster sizes given on the command line; traces must agree across C."""
 import json, os, sys
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_1910_06451_b200 as fb, workloads as W
 tw = W.train_workload()
