@@ -85,3 +85,16 @@ def test_fk_maximum_dof_and_control_points():
     robot = W.make_robot("d16m32", dh, rng.integers(0, 17, size=32), rng.uniform(-0.1, 0.1, size=(32, 3)))
     q = rng.uniform(-np.pi, np.pi, size=(777, 16)).astype(np.float32)
     _check(robot, q)
+
+
+def test_fk_large_angles():
+    """Joint values far outside [-pi, pi]: the table sincos's Cody-Waite reduction (|k pi/64|
+    up to ~5e4 rad here) and, past 1e6 multiples of pi/64, its fall-back to the library
+    sincos keep positions within one fp32 ulp of the oracle."""
+    require_gpu()
+    robot = W.arm7(8)
+    rng = np.random.default_rng(7)
+    q = np.concatenate([rng.uniform(-1000, 1000, size=(500, 7)), rng.uniform(-5e4, 5e4, size=(200, 7)),
+                        rng.uniform(2e4, 2.5e4, size=(100, 7)) * rng.choice([-1, 1], size=(100, 7)),
+                        np.full((1, 7), np.float32(np.pi)), np.full((1, 7), np.float32(-np.pi / 2))]).astype(np.float32)
+    _check(robot, q, atol=2e-6)
