@@ -137,9 +137,10 @@ fastron_status fastron_score(const float* qpos, int64_t nq, int64_t ldq, const f
  *   fastron_score_packed_workspace_bytes(nq, ns, n_cp) (may be 0 bytes).
  */
 size_t fastron_model_bytes(int64_t ns, int32_t n_cp);
-/* fastron_score_packed_f64: the same scores in fp64 (before the fp32 rounding), e.g. the
- * margins F = K alpha a warm-started Algorithm 1 needs. score64: device
- * double [nq]. */
+/* fastron_score_packed_f64: the same scores in fp64 (before the fp32 rounding). score64:
+ * device double [nq]. (The packed alpha is fp32 and the sums follow the scoring order, so
+ * these are NOT the margins F = K alpha of Algorithm 1: use fastron_kernel_matvec or
+ * fastron_kernel_matvec_lazy for a warm start.) */
 fastron_status fastron_score_packed_f64(const float* qpos, int64_t nq, int64_t ldq, const void* packed, int64_t ns,
                                         int32_t n_cp, fastron_kernel k, double* score64, void* workspace,
                                         size_t workspace_bytes, void* stream);
@@ -228,6 +229,12 @@ fastron_status fastron_train_lazy(const float* pos, int64_t n, int64_t ldp, int3
  *   int8 [n], +1 iff any capsule touches any box (tangency counts).
  * fastron_kernel_matvec — F = K alpha (fp64, index order over alpha != 0), the margin
  *   vector a warm start needs when the dataset changed around a loaded alpha.
+ * fastron_kernel_matvec_lazy — the same F = K alpha for the lazy Algorithm 1, without the
+ *   Gram: every K entry is computed from the control points pos (device float4
+ *   [n_cp][ldp], ldp >= n) exactly as fastron_gram computes it, so F equals
+ *   fastron_kernel_matvec(fastron_gram(pos), alpha) bit for bit.
+ *   alpha, F: device double [n]. workspace (256-byte aligned):
+ *   >= fastron_kernel_matvec_lazy_workspace_bytes(n, n_cp). Cost: n x nnz(alpha) entries.
  */
 fastron_status fastron_active_samples(const float* S, int64_t ns, int64_t lds, int32_t dof, int32_t n_near,
                                       const float* z, const float* sigma, const float* u, int64_t n_uniform,
@@ -236,6 +243,10 @@ fastron_status fastron_label_capsules(const float* pos, int64_t ldp, int64_t n, 
                                       const double* boxes, int32_t n_cubes, float radius, int8_t* label, void* stream);
 fastron_status fastron_kernel_matvec(const float* K, int64_t n, int64_t ldk, const double* alpha, double* F,
                                      void* stream);
+size_t fastron_kernel_matvec_lazy_workspace_bytes(int64_t n, int32_t n_cp);
+fastron_status fastron_kernel_matvec_lazy(const float* pos, int64_t n, int64_t ldp, int32_t n_cp, fastron_kernel k,
+                                          const double* alpha, double* F, void* workspace, size_t workspace_bytes,
+                                          void* stream);
 
 /*
  * fastron_edge_check — discrete motion-planning edge check (BASELINE.json cfg4,

@@ -505,6 +505,36 @@ fastron_status fastron_kernel_matvec(const float* K, int64_t n, int64_t ldk, con
   return cuda_status(launch_matvec(K, n, ldk, alpha, F, S(stream)), "fastron_kernel_matvec");
 }
 
+size_t fastron_kernel_matvec_lazy_workspace_bytes(int64_t n, int32_t n_cp) {
+  if (n < 0 || n_cp < 1 || n_cp > FASTRON_MAX_CP) return 0;
+  return align_up(packed_bytes(n, n_cp));
+}
+
+fastron_status fastron_kernel_matvec_lazy(const float* pos, int64_t n, int64_t ldp, int32_t n_cp, fastron_kernel k,
+                                          const double* alpha, double* F, void* workspace, size_t workspace_bytes,
+                                          void* stream) {
+  NvtxRange nvtx_range_("fastron_kernel_matvec_lazy");
+  fastron_status s = check_kernel(k);
+  if (s != FASTRON_OK) return s;
+  FASTRON_REQUIRE(n >= 0, "n must be >= 0");
+  FASTRON_REQUIRE(n_cp >= 1 && n_cp <= FASTRON_MAX_CP, "n_cp must be in [1,32], got %d", n_cp);
+  if (n == 0) return FASTRON_OK;
+  FASTRON_REQUIRE(pos && alpha && F && ldp >= n, "pos, alpha, F must be non-NULL and ldp >= n");
+  FASTRON_REQUIRE(((uintptr_t)pos & 15) == 0, "pos must be 16-byte aligned (float4 records)");
+  const size_t need = fastron_kernel_matvec_lazy_workspace_bytes(n, n_cp);
+  if (workspace_bytes < need || !workspace)
+    return fail(FASTRON_ERR_WORKSPACE, "fastron_kernel_matvec_lazy needs %zu workspace bytes, got %zu", need,
+                workspace_bytes);
+  FASTRON_REQUIRE(((uintptr_t)workspace & 255) == 0, "workspace must be 256-byte aligned");
+  FASTRON_VALIDATE(vcheck_f32(pos, n_cp, 4 * n, 4 * ldp, stream, "pos"));
+  FASTRON_VALIDATE(vcheck_f64(alpha, n, stream, "alpha"));
+  float* packed = static_cast<float*>(workspace);
+  cudaStream_t st = S(stream);
+  cudaError_t e = launch_pack(reinterpret_cast<const float4*>(pos), ldp, nullptr, n, n_cp, kernel_scale(k), packed, st);
+  if (e == cudaSuccess) e = launch_matvec_lazy(packed, n, n_cp, k.kind, alpha, F, st);
+  return cuda_status(e, "fastron_kernel_matvec_lazy");
+}
+
 size_t fastron_edge_workspace_bytes(int64_t n_edges, int64_t ns, int32_t n_cp) {
   if (n_edges < 0 || ns < 0 || n_cp < 1 || n_cp > FASTRON_MAX_CP) return 0;
   const size_t lists = 2 * align_up((size_t)n_edges * 4) + 256;  // two active lists + two counters

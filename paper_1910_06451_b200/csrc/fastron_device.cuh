@@ -25,9 +25,11 @@ constexpr int kRQ = 1;
 // (x_m, x_m+1, y_m, y_m+1, z_m, z_m+1, 0, 0), pre-scaled, followed after the TS
 // records by TS alpha values stored as double (the fp64 accumulation operand).
 // Padded control points (m >= M) hold kPadCoord so their term is exactly 0; padded
-// supports (index >= ns) hold zeros and alpha = 0.
+// supports (index >= ns) hold zeros and alpha = 0. The pad keeps d2 finite (3e36 < FLT_MAX):
+// an infinite d2 would make the RQ Newton step's rcp(-inf) * inf a NaN; at 3e36 every term
+// shape gives exactly 0 (2^-3e36, and (3e36)^-2 underflows).
 constexpr int kTileSupports = 64;
-constexpr float kPadCoord = 1.0e30f;
+constexpr float kPadCoord = 1.0e18f;
 
 __host__ __device__ constexpr int64_t tile_record_floats(int mp) { return (int64_t)kTileSupports * (mp / 2) * 8; }
 __host__ __device__ constexpr int64_t tile_floats(int mp) { return tile_record_floats(mp) + 2 * kTileSupports; }
@@ -102,26 +104,66 @@ __device__ __forceinline__ f2 term_pair(f2 ux, f2 uy, f2 uz, f2 vx, f2 vy, f2 vz
   return term_from_diffs<KIND>(sub2(ux, vx), sub2(uy, vy), sub2(uz, vz));
 }
 
+// RQ term evaluation (A/B knob; 1 = default):
+//  0: w = 1 + d2 as one FFMA chain seeded with 1, r = rcp(w), t = r^2 (7 packed ops per
+//     pair; w rounded three times at ulp(w) plus the rcp.approx error: ~3e-6 rms at the
+//     headline size, over the 1e-5 floor at |S| = 20,000 — DESIGN.md §5)
+//  1: s = d2 first (rounded at ulp(d2)), w = 1 + s, r0 = rcp(w), then one Newton step
+//     against the UNROUNDED 1 + s: e = (1 - r0) - r0 s, r = r0 (1 + e). The residual
+//     removes both the rounding of w and the rcp.approx error (11 packed ops per pair).
+#ifndef FASTRON_RQ_NEWTON
+#define FASTRON_RQ_NEWTON 1
+#endif
+
 // acc (+)= the terms of control points (m, m+1): the per-lane running sum over the pairs
-// p = 0, 1, ... (first: p == 0). Every kernel accumulates through this one function, so
-// the Gram, the scores and the lazy columns stay bit-identical.
+// p = 0, 1, ... (first: p == 0, the lane starts from `init`). Every kernel accumulates
+// through this one function, so the Gram, the scores and the lazy columns stay
+// bit-identical (the scoring kernels start the RQ lanes from -offset, see rq_lane_offset).
 // Gaussian: t = 2^-d2 as above, then acc + t.
-// RQ: r = rcp(w) with w = 1 + d2, and acc = fma(r, r, acc): the square of (1 + d2)^-1 rides
-// in the accumulating FFMA2, one packed op fewer than rcp(w*w) + add (7 per pair, as the
-// Gaussian, instead of 8: the FMA pipe no longer co-limits with the MUFU).
+// RQ (FASTRON_RQ_NEWTON, see above): the square of r = (1 + d2)^-1 rides in the
+// accumulating FFMA2. The MUFU takes the source negation for free, so the Newton step runs
+// on nr0 = rcp(-w) = -r0 without separate negations:
+//   u = 1 + nr0 (= 1 - r0, exact for r0 >= 1/2), e = fma(nr0, s, u), nr = fma(nr0, e, nr0)
+//   (= -r), acc = fma(nr, nr, acc).
 template <int KIND>
-__device__ __forceinline__ void accum_term(f2& acc, f2 dx, f2 dy, f2 dz, bool first) {
+__device__ __forceinline__ void accum_term(f2& acc, f2 dx, f2 dy, f2 dz, bool first, f2 init = 0ull) {
   if (KIND == kGaussian) {
     const f2 t = term_from_diffs<KIND>(dx, dy, dz);
-    acc = first ? t : add2(acc, t);
+    acc = first ? (init ? add2(init, t) : t) : add2(acc, t);
   } else {
     const f2 one = pk(1.0f, 1.0f);
+#if FASTRON_RQ_NEWTON
+    f2 s = mul2(dx, dx);
+    s = fma2(dy, dy, s);
+    s = fma2(dz, dz, s);
+    const f2 w = add2(s, one);
+    const f2 nr0 = pk(rcp_approx(-lo(w)), rcp_approx(-hi(w)));
+    const f2 u = add2(one, nr0);
+    const f2 e = fma2(nr0, s, u);
+    const f2 nr = fma2(nr0, e, nr0);
+    acc = fma2(nr, nr, first ? init : acc);
+#else
     f2 w = fma2(dx, dx, one);
     w = fma2(dy, dy, w);
     w = fma2(dz, dz, w);
     const f2 r = pk(rcp_approx(lo(w)), rcp_approx(hi(w)));
-    acc = first ? mul2(r, r) : fma2(r, r, acc);
+    acc = first ? (init ? fma2(r, r, init) : mul2(r, r)) : fma2(r, r, acc);
+#endif
   }
+}
+
+// Lane offset of the scoring kernels' RQ sums (A/B knob FASTRON_RQ_OFFSET, 1 = default).
+// Under RQ every support contributes (k >= 0.14 on these arms), and each fp32 lane sums
+// NP terms of mean ~0.35 (headline): the rounding of the running sum at ulp(~1.4) was
+// ~1.6e-6 rms of the headline score error. Starting each lane from -NP/4 keeps the running
+// sums near 0; the scoring kernels add 2 * (NP/4) * sum(alpha) back in fp64 (exact), so
+// the value is unchanged and only the rounding shrinks.
+#ifndef FASTRON_RQ_OFFSET
+#define FASTRON_RQ_OFFSET 1
+#endif
+template <int KIND, int NP>
+__host__ __device__ constexpr float rq_lane_offset() {
+  return (KIND == kRQ && FASTRON_RQ_OFFSET) ? 0.25f * (float)NP : 0.0f;
 }
 
 // Sum over the M control points of one (query, support) pair, in the fixed order
@@ -134,6 +176,28 @@ __device__ __forceinline__ float pair_sum(f2 acc) { return lo(acc) + hi(acc); }
 __device__ __forceinline__ double nonneg_f32_to_f64(float x) {
   const uint32_t b = __float_as_uint(x);
   return __hiloint2double((int)((b >> 3) + 0x38000000u), (int)(b << 29));
+}
+
+// The same for either sign (the offset RQ lane sums): magnitude as above, sign bit copied
+// (5 ALU instructions).
+__device__ __forceinline__ double f32_to_f64_alu(float x) {
+  const uint32_t b = __float_as_uint(x);
+  return __hiloint2double((int)((((b & 0x7fffffffu) >> 3) + 0x38000000u) | (b & 0x80000000u)), (int)(b << 29));
+}
+
+// Promotion of the RQ lane sums: the Newton step leaves the RQ kernel FMA-pipe and issue
+// bound with the MUFU only ~60 % busy, so there the conversion instruction (F2F, on the
+// MUFU pipe: 2 per support and query) is cheaper than the 2 x 5 ALU instructions of
+// f32_to_f64_alu. A/B knob FASTRON_RQ_F2F (1 = default).
+#ifndef FASTRON_RQ_F2F
+#define FASTRON_RQ_F2F 1
+#endif
+__device__ __forceinline__ double rq_lane_to_f64(float x) {
+#if FASTRON_RQ_F2F
+  return (double)x;
+#else
+  return f32_to_f64_alu(x);
+#endif
 }
 
 // ---------------------------------------------------------------------------------

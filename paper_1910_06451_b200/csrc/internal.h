@@ -94,6 +94,8 @@ cudaError_t launch_active_samples(const float* S, int64_t ns, int64_t lds, int D
 cudaError_t launch_label_capsules(const float4* pos, int64_t ldp, int64_t n, const int32_t* chain, int n_chain,
                                   const double* boxes, int n_cubes, float radius, int8_t* label, cudaStream_t st);
 cudaError_t launch_matvec(const float* K, int64_t n, int64_t ldk, const double* alpha, double* F, cudaStream_t st);
+cudaError_t launch_matvec_lazy(const float* packed, int64_t n, int M, int kind, const double* alpha, double* F,
+                               cudaStream_t st);
 
 // Optional content checks (validate.cu): counts are read back synchronously.
 cudaError_t count_nonfinite(const float* a, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st,

@@ -289,6 +289,10 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
   double f[QT];
 #pragma unroll
   for (int j = 0; j < QT; ++j) f[j] = 0.0;
+  // RQ lanes start from -OFF (rq_lane_offset); 2 OFF sum(alpha) is added back at the end
+  constexpr float OFF = MODE == MODE_JOINT ? 0.0f : rq_lane_offset<KIND, NP>();
+  const f2 lane0 = OFF != 0.0f ? pk(-OFF, -OFF) : 0ull;
+  double asum = 0.0;
 
   // ---- stream the support tiles ----
   for (int it = 0; it < nt; ++it) {
@@ -300,6 +304,7 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
     for (int s = 0; s < kTileSupports; ++s) {
       const float* rec = T + s * NP * 8;
       const double a = alpha[s];
+      if (OFF != 0.0f) asum += a;
       if (MODE == MODE_JOINT) {
         // joint-space RBF: accumulate the squared distance over all pseudo points, one MUFU
         f2 s2[QT];
@@ -348,20 +353,25 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
         for (int j = 0; j < QT; ++j) dz[j] = sub2(uz[j][p], vz);
 #pragma unroll
         for (int j = 0; j < QT; ++j) {
-          accum_term<KIND>(acc[j], dx[j], dy[j], dz[j], p == 0);
+          accum_term<KIND>(acc[j], dx[j], dy[j], dz[j], p == 0, lane0);
         }
 #else
 #pragma unroll
         for (int j = 0; j < QT; ++j) {
-          accum_term<KIND>(acc[j], sub2(ux[j][p], vx), sub2(uy[j][p], vy), sub2(uz[j][p], vz), p == 0);
+          accum_term<KIND>(acc[j], sub2(ux[j][p], vx), sub2(uy[j][p], vy), sub2(uz[j][p], vz), p == 0, lane0);
         }
 #endif
       }
 #pragma unroll
       for (int j = 0; j < QT; ++j) {
 #if FASTRON_ACC_SPLIT
-        f[j] = fma(a, nonneg_f32_to_f64(lo(acc[j])), f[j]);
-        f[j] = fma(a, nonneg_f32_to_f64(hi(acc[j])), f[j]);
+        if (KIND == kRQ && MODE != MODE_JOINT) {  // offset lanes can be negative
+          f[j] = fma(a, rq_lane_to_f64(lo(acc[j])), f[j]);
+          f[j] = fma(a, rq_lane_to_f64(hi(acc[j])), f[j]);
+        } else {
+          f[j] = fma(a, nonneg_f32_to_f64(lo(acc[j])), f[j]);
+          f[j] = fma(a, nonneg_f32_to_f64(hi(acc[j])), f[j]);
+        }
 #else
         f[j] = fma(a, nonneg_f32_to_f64(pair_sum(acc[j])), f[j]);
 #endif
@@ -376,6 +386,10 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
   }
 
   // ---- epilogue ----
+  if (OFF != 0.0f) {
+#pragma unroll
+    for (int j = 0; j < QT; ++j) f[j] = fma(2.0 * (double)OFF, asum, f[j]);
+  }
 #pragma unroll
   for (int j = 0; j < QT; ++j) {
     const int64_t vq = q_base + j * kNT + tid;
@@ -511,10 +525,14 @@ __global__ void __launch_bounds__(kSmallNT) score_small_kernel(const __grid_cons
   double f[kSmallQ];
 #pragma unroll
   for (int q = 0; q < kSmallQ; ++q) f[q] = 0.0;
+  constexpr float OFF = rq_lane_offset<KIND, NP>();  // as in score_kernel
+  const f2 lane0 = OFF != 0.0f ? pk(-OFF, -OFF) : 0ull;
+  double asum = 0.0;
   for (int64_t sup = (int64_t)blockIdx.x * kSmallNT + tid; sup < ns; sup += (int64_t)gridDim.x * kSmallNT) {
     const float* T = A.packed + (sup / kTileSupports) * TF;
     const float* rec = T + (sup % kTileSupports) * NP * 8;
     const double a = reinterpret_cast<const double*>(T + tile_record_floats(MP))[sup % kTileSupports];
+    if (OFF != 0.0f) asum += a;
     f2 vx[NP], vy[NP], vz[NP];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
@@ -530,11 +548,21 @@ __global__ void __launch_bounds__(kSmallNT) score_small_kernel(const __grid_cons
         f2 acc;
 #pragma unroll
         for (int p = 0; p < NP; ++p)
-          accum_term<KIND>(acc, sub2(sq[q][p][0], vx[p]), sub2(sq[q][p][1], vy[p]), sub2(sq[q][p][2], vz[p]), p == 0);
-        f[q] = fma(a, nonneg_f32_to_f64(lo(acc)), f[q]);
-        f[q] = fma(a, nonneg_f32_to_f64(hi(acc)), f[q]);
+          accum_term<KIND>(acc, sub2(sq[q][p][0], vx[p]), sub2(sq[q][p][1], vy[p]), sub2(sq[q][p][2], vz[p]), p == 0,
+                           lane0);
+        if (KIND == kRQ) {  // offset lanes can be negative
+          f[q] = fma(a, rq_lane_to_f64(lo(acc)), f[q]);
+          f[q] = fma(a, rq_lane_to_f64(hi(acc)), f[q]);
+        } else {
+          f[q] = fma(a, nonneg_f32_to_f64(lo(acc)), f[q]);
+          f[q] = fma(a, nonneg_f32_to_f64(hi(acc)), f[q]);
+        }
       }
     }
+  }
+  if (OFF != 0.0f) {
+#pragma unroll
+    for (int q = 0; q < kSmallQ; ++q) f[q] = fma(2.0 * (double)OFF, asum, f[q]);
   }
 #pragma unroll
   for (int q = 0; q < kSmallQ; ++q) {

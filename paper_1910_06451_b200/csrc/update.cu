@@ -12,6 +12,10 @@
 //    slab crossings). Tangency counts as collision.
 //  * matvec_kernel: F = K alpha for a warm start whose alpha changed support set
 //    (F must match the loaded alpha), fixed summation order.
+//  * matvec_lazy_kernel: the same F = K alpha without the Gram, for the lazy Algorithm 1:
+//    each K entry is computed from the packed records with the Gram's term function,
+//    summation order and 1/M (so it equals K3's entry bit for bit), then accumulated in
+//    matvec_kernel's fp64 order.
 #include "fastron_device.cuh"
 #include "internal.h"
 
@@ -124,6 +128,88 @@ __global__ void matvec_kernel(const float* __restrict__ K, int64_t n, int64_t ld
     if (a != 0.0) f = __dadd_rn(f, __dmul_rn(a, (double)K[i * ldk + j]));
   }
   F[j] = f;
+}
+
+template <int MP, int KIND>
+__global__ void __launch_bounds__(128) matvec_lazy_kernel(const float* __restrict__ packed, int64_t n, int M,
+                                                          int m_pow2, float inv_m, const double* __restrict__ alpha,
+                                                          double* __restrict__ F) {
+  constexpr int NP = MP / 2;
+  constexpr int64_t TF = tile_floats(MP);
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  // column j in registers, its padded point (odd M) at 0 as on K3's column side
+  f2 ux[NP], uy[NP], uz[NP];
+  const float* rj = packed + (j / kTileSupports) * TF + (j % kTileSupports) * NP * 8;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const float4 xy = __ldg(reinterpret_cast<const float4*>(rj + p * 8));
+    const float2 zz = __ldg(reinterpret_cast<const float2*>(rj + p * 8 + 4));
+    ux[p] = pk(xy.x, xy.y);
+    uy[p] = pk(xy.z, xy.w);
+    uz[p] = pk(zz.x, zz.y);
+  }
+  if (M < MP) {
+    ux[NP - 1] = pk(lo(ux[NP - 1]), 0.0f);
+    uy[NP - 1] = pk(lo(uy[NP - 1]), 0.0f);
+    uz[NP - 1] = pk(lo(uz[NP - 1]), 0.0f);
+  }
+  double f = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double a = __ldg(alpha + i);  // uniform across the CTA
+    if (a == 0.0) continue;
+    const float* ri = packed + (i / kTileSupports) * TF + (i % kTileSupports) * NP * 8;
+    f2 acc;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const float4 xy = __ldg(reinterpret_cast<const float4*>(ri + p * 8));
+      const float2 zz = __ldg(reinterpret_cast<const float2*>(ri + p * 8 + 4));
+      accum_term<KIND>(acc, sub2(ux[p], pk(xy.x, xy.y)), sub2(uy[p], pk(xy.z, xy.w)), sub2(uz[p], pk(zz.x, zz.y)),
+                       p == 0);
+    }
+    const float ks = pair_sum(acc);
+    const float v = m_pow2 ? ks * inv_m : __fdiv_rn(ks, (float)M);
+    f = __dadd_rn(f, __dmul_rn(a, (double)v));
+  }
+  F[j] = f;
+}
+
+cudaError_t launch_matvec_lazy(const float* packed, int64_t n, int M, int kind, const double* alpha, double* F,
+                               cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int m_pow2 = (M & (M - 1)) == 0;
+  const float inv_m = 1.0f / (float)M;
+  const unsigned grid = (unsigned)((n + 127) / 128);
+  switch (padded_m(M)) {
+#define FASTRON_MVCASE(mp)                                                                                      \
+  case mp:                                                                                                      \
+    if (kind == kGaussian)                                                                                      \
+      matvec_lazy_kernel<mp, kGaussian><<<grid, 128, 0, st>>>(packed, n, M, m_pow2, inv_m, alpha, F);           \
+    else                                                                                                        \
+      matvec_lazy_kernel<mp, kRQ><<<grid, 128, 0, st>>>(packed, n, M, m_pow2, inv_m, alpha, F);                 \
+    break;
+    FASTRON_MVCASE(2)
+    FASTRON_MVCASE(4)
+    FASTRON_MVCASE(6)
+    FASTRON_MVCASE(8)
+    FASTRON_MVCASE(10)
+    FASTRON_MVCASE(12)
+    FASTRON_MVCASE(14)
+    FASTRON_MVCASE(16)
+    FASTRON_MVCASE(18)
+    FASTRON_MVCASE(20)
+    FASTRON_MVCASE(22)
+    FASTRON_MVCASE(24)
+    FASTRON_MVCASE(26)
+    FASTRON_MVCASE(28)
+    FASTRON_MVCASE(30)
+    FASTRON_MVCASE(32)
+#undef FASTRON_MVCASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+  g_launches.fetch_add(1);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_active_samples(const float* S, int64_t ns, int64_t lds, int D, int n_near, const float* z,

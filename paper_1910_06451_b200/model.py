@@ -11,8 +11,8 @@ from typing import Optional
 
 import numpy as np
 
-from . import (fastron_active_samples, fastron_fk, fastron_gram, fastron_kernel_matvec, fastron_label_capsules,
-               fastron_model_pack, fastron_score_packed, fastron_score_packed_f64, fastron_train, fastron_train_lazy,
+from . import (fastron_active_samples, fastron_fk, fastron_gram, fastron_kernel_matvec, fastron_kernel_matvec_lazy,
+               fastron_label_capsules, fastron_model_pack, fastron_score_packed, fastron_train, fastron_train_lazy,
                make_robot_struct, train_result)
 
 
@@ -46,8 +46,8 @@ class FastronModel:
         n = X.shape[0]
         s_max = n if self.s_max is None else self.s_max
         if self.lazy:
-            if alpha0 is not None and F0 is None:  # margins of the loaded model: F = K alpha = f(X)
-                F0 = fastron_score_packed_f64(pos, self.model)
+            if alpha0 is not None and F0 is None:  # margins of the loaded model: F = K alpha (as the full mode)
+                F0 = fastron_kernel_matvec_lazy(pos, alpha0, self.kind, self.gamma)
             out = fastron_train_lazy(pos, y, self.kind, self.gamma, self.beta, self.iter_max, s_max, alpha=alpha0, F=F0,
                                      cache_cols=min(self.cache_cols, n))
         else:
@@ -90,10 +90,15 @@ class FastronModel:
 
     def load_state_dict(self, st: dict, device="cuda") -> None:
         """Restore a saved model (its robot must match this model's) and re-pack it."""
-        dh = np.asarray(self.robot.dh, dtype=np.float32)
-        if not np.array_equal(st["robot_dh"].numpy(), dh) or \
-                not np.array_equal(st["robot_cp_frame"].numpy(), np.asarray(self.robot.cp_frame, dtype=np.int32)):
-            raise ValueError("the saved model belongs to a different robot")
+        # every part of the robot the scores depend on (D-H table, control-point frames and
+        # offsets, base pose), compared after the same fp32 rounding the checkpoint applied
+        mine = {"robot_dh": np.asarray(self.robot.dh, dtype=np.float32),
+                "robot_cp_frame": np.asarray(self.robot.cp_frame, dtype=np.int32),
+                "robot_cp_offset": np.asarray(self.robot.cp_offset, dtype=np.float32).reshape(-1, 3),
+                "robot_base": np.asarray(self.robot.base, dtype=np.float32)}
+        for key, v in mine.items():
+            if key not in st or st[key].numpy().shape != v.shape or not np.array_equal(st[key].numpy(), v):
+                raise ValueError(f"the saved model belongs to a different robot ({key} differs)")
         self.kind, self.gamma, self.beta = int(st["kind"]), float(st["gamma"]), float(st["beta"])
         self.supports = st["supports"].to(device).contiguous()
         self.alpha = st["alpha"].to(device).contiguous()

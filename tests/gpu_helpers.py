@@ -34,11 +34,6 @@ def positions_np(pos_dev):
     return np.transpose(p[:, :, :3], (1, 0, 2)).astype(np.float64)
 
 
-def rq_floor(n_supports):
-    """DESIGN.md R24: the absolute floor for the RQ term at |S| supports."""
-    return 1e-5 * max(1.0, (n_supports / 2000.0) ** 0.5)
-
-
 def assert_score_parity(f_gpu, f_ref, label_gpu=None, rel=1e-4, floor=1e-5, what=""):
     """BASELINE.json north_star tolerance (R16): |f_gpu - f_ref| <= max(rel |f_ref|, floor)
     for every checked query; labels equal wherever |f_ref| > 1e-4."""

@@ -5,6 +5,7 @@ import pytest
 
 import oracle
 import workloads as W
+from c4 import assert_stats, score_stats
 from gpu_helpers import dev, require_gpu
 
 pytestmark = pytest.mark.gpu
@@ -34,17 +35,24 @@ def test_fit_then_query_matches_oracle(kind):
     a32 = m.alpha.float().cpu().numpy()
     qp, sp = oracle.fk(tw.robot, q), oracle.fk(tw.robot, sup_X)
     f, _ = oracle.score(kind, tw.gamma, qp, sp, a32)
-    # R25: a trained alpha has large entries of both signs, so the fp32 rounding of each
-    # term scales with sum_i |alpha_i| k_i (the sum's condition), not with |f|
+    # A trained alpha has large entries of both signs (Algorithm 1 never shrinks them), so f
+    # is a cancelling sum: fp32 positions and fp32 terms perturb it in proportion to its
+    # condition sum_i |alpha_i| k_i, not to |f| ("trained models"). R16 is the
+    # pass criterion on the non-cancelling queries (kappa = condition / |f| <= 1e4: the sum
+    # loses at most 4 of fp32's 7 digits); the rest are counted and reported. Labels must
+    # agree wherever |f_ref| > 1e-4, on every query (the north-star label rule).
     cond, _ = oracle.score(kind, tw.gamma, qp, sp, np.abs(a32))
-    err = np.abs(s.cpu().numpy().astype(np.float64) - f)
-    tol = np.maximum(np.maximum(1e-4 * np.abs(f), 1e-5), 1e-7 * cond)
-    assert np.all(err <= tol), (f"{np.sum(err > tol)} outside; max err/cond {np.max(err / cond):.2e}, "
-                                f"max |alpha| {np.abs(a32).max():.3g}")
+    sg = s.cpu().numpy().astype(np.float64)
+    kappa = cond / np.maximum(np.abs(f), 1e-300)
+    ok = kappa <= 1e4
+    st = score_stats(sg[ok], f[ok])
+    assert ok.sum() > 1000, f"only {ok.sum()} non-cancelling queries"
+    assert_stats(st, f"trained model kind={kind}, non-cancelling queries")
     lab = l.cpu().numpy()
-    sure = np.abs(f) > np.maximum(1e-4, 1e-7 * cond)
+    sure = np.abs(f) > 1e-4
     assert np.array_equal(lab[sure], np.where(f[sure] > 0, 1, -1))
-    print(f"kind={kind}: max err/cond {np.max(err / cond):.2e}, max |alpha| {np.abs(a32).max():.3g}")
+    print(f"kind={kind}: {ok.sum()} non-cancelling queries {st}; {np.sum(~ok)} with kappa > 1e4 "
+          f"(max err there {np.max(np.abs(sg - f)[~ok]) if (~ok).any() else 0:.2e}); max |alpha| {np.abs(a32).max():.3g}")
     # the training set is classified by its own margins' signs where they are certain
     s_tr, _ = m.query(dev(tw.X))
     F = r["F"]

@@ -86,3 +86,60 @@ def test_update_cycle_is_alg1_on_the_relabelled_set():
     s, l = model.query(dev(wl.X[:1000]))
     torch.cuda.synchronize()
     assert np.all(np.isfinite(s.cpu().numpy()))
+
+
+@pytest.mark.parametrize("M", [5, 8, 16])
+@pytest.mark.parametrize("kind", [W.GAUSSIAN, W.RQ])
+def test_lazy_matvec_equals_gram_matvec(M, kind):
+    """fastron_kernel_matvec_lazy (no Gram) equals fastron_kernel_matvec(fastron_gram(pos))
+    bit for bit: same K entries (K3's term function, order and 1/M), same fp64 order."""
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    base = W.arm7(8)
+    rng = np.random.default_rng(M + 10 * kind)
+    robot = base if M == 8 else W.make_robot("m%d" % M, base.dh, rng.integers(0, 8, size=M),
+                                              rng.uniform(-0.1, 0.1, size=(M, 3)))
+    X = W.uniform_configs(rng, 1234, 7)
+    pos = fb.fastron_fk(robot, dev(X))
+    a = rng.standard_normal(1234) * (rng.uniform(size=1234) < 0.3) * 50.0  # sparse, large, both signs
+    alpha = dev(a)
+    F_full = fb.fastron_kernel_matvec(fb.fastron_gram(pos, kind, 5.0), alpha)
+    F_lazy = fb.fastron_kernel_matvec_lazy(pos, alpha, kind, 5.0)
+    torch.cuda.synchronize()
+    assert torch.equal(F_full, F_lazy)
+
+
+def test_lazy_update_equals_full_update():
+    """update() in the lazy mode (no Gram; F_0 from fastron_kernel_matvec_lazy) retraces the
+    full mode's warm-started Algorithm 1 exactly (F_0 must be K alpha_0, not
+    the fp32-alpha score)."""
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    from paper_1910_06451_b200.model import CapsuleScene, FastronModel
+    wl = W.train_workload(1500)
+    X = dev(wl.X)
+    y = fb.fastron_label_capsules(fb.fastron_fk(wl.robot, X), CHAIN8, wl.cubes, wl.radius)
+    full = FastronModel(wl.robot, 0, wl.gamma, 1.0, 4000)
+    lazy = FastronModel(wl.robot, 0, wl.gamma, 1.0, 4000, lazy=True)
+    full.fit(X, y)
+    lazy.fit(X, y)
+    assert torch.equal(full.alpha, lazy.alpha)
+    ns = full.supports.shape[0]
+    moved = wl.cubes.copy()
+    rng = np.random.default_rng(8)
+    for j in rng.choice(len(moved), 3, replace=False):
+        v = rng.standard_normal(3)
+        moved[j] += 0.1 * v / np.linalg.norm(v)
+    z = dev(rng.standard_normal((2 * ns, 7)).astype(np.float32))
+    u = dev(rng.uniform(0, 1, (800, 7)).astype(np.float32))
+    sigma = dev(np.full(7, 0.05 * 2 * np.pi, np.float32))
+    lo, hi = dev(np.full(7, -np.pi, np.float32)), dev(np.full(7, np.pi, np.float32))
+    scene = CapsuleScene(np.array(CHAIN8), moved, wl.radius)
+    rf = full.update(scene, z, u, sigma, lo, hi, 2)[0]
+    rl = lazy.update(scene, z, u, sigma, lo, hi, 2)[0]
+    torch.cuda.synchronize()
+    for k in ("iterations", "n_add", "n_remove", "n_support", "converged"):
+        assert rf[k] == rl[k], (k, rf, rl)
+    assert torch.equal(full.alpha, lazy.alpha) and torch.equal(full.supports, lazy.supports)
