@@ -302,6 +302,25 @@ fastron_status fastron_query(const fastron_robot* robot, const float* q, int64_t
                              const float* alpha, int64_t ns, int64_t lds, fastron_kernel k, float* score,
                              int8_t* label, void* workspace, size_t workspace_bytes, void* stream);
 
+/*
+ * fastron_query_packed — the proxy collision check of configurations against a model
+ * packed once by fastron_model_pack (the planner's call: configurations
+ * in, scores and labels out, one API call per batch). DEVICE buffers only (fastron_query
+ * streams host buffers). For nq <= 32 (n_cp <= 16) it is one launch of the
+ * support-parallel kernel with the D-H chain inside; otherwise fastron_fk +
+ * fastron_score_packed on the workspace. Every path gives the bits of fastron_fk +
+ * fastron_score_packed on the same batch.
+ *   robot: host; n_cp must equal robot->n_cp and the packing's n_cp. q: device float
+ *   [nq][ldq], ldq >= dof. packed: device, 256-byte aligned (fastron_model_pack).
+ *   score / label: device, nullable (not both). workspace (256-byte aligned):
+ *   >= fastron_query_packed_workspace_bytes(nq, ns, n_cp, dof).
+ *   Errors: host pointers -> INVALID_ARG.
+ */
+size_t fastron_query_packed_workspace_bytes(int64_t nq, int64_t ns, int32_t n_cp, int32_t dof);
+fastron_status fastron_query_packed(const fastron_robot* robot, const float* q, int64_t nq, int64_t ldq,
+                                    const void* packed, int64_t ns, int32_t n_cp, fastron_kernel k, float* score,
+                                    int8_t* label, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Thread-local message for the last non-OK status returned on this thread. */
 const char* fastron_last_error(void);
 

@@ -34,6 +34,7 @@ EXPORTED = [
     "fastron_train_lazy_workspace_bytes", "fastron_train_lazy", "fastron_active_samples", "fastron_label_capsules",
     "fastron_kernel_matvec", "fastron_score_packed_f64", "fastron_set_validation", "fastron_validation",
     "fastron_kernel_matvec_lazy_workspace_bytes", "fastron_kernel_matvec_lazy",
+    "fastron_query_packed_workspace_bytes", "fastron_query_packed",
 ]
 
 
@@ -119,10 +120,13 @@ def load_library(path: str = LIB_PATH):
     L.fastron_query_workspace_bytes.argtypes = [i64, i64, i32, i32]
     L.fastron_query_workspace_bytes.restype = sz
     L.fastron_query.argtypes = [rp, vp, i64, i64, vp, vp, i64, i64, fastron_kernel, vp, vp, vp, sz, vp]
+    L.fastron_query_packed_workspace_bytes.argtypes = [i64, i64, i32, i32]
+    L.fastron_query_packed_workspace_bytes.restype = sz
+    L.fastron_query_packed.argtypes = [rp, vp, i64, i64, vp, i64, i32, fastron_kernel, vp, vp, vp, sz, vp]
     for f in ("fastron_fk", "fastron_score", "fastron_gram", "fastron_train", "fastron_edge_check", "fastron_query",
               "fastron_model_pack", "fastron_score_packed", "fastron_score_joint", "fastron_gram_joint", "fastron_train_lazy", "fastron_active_samples",
               "fastron_label_capsules", "fastron_kernel_matvec", "fastron_score_packed_f64",
-              "fastron_kernel_matvec_lazy"):
+              "fastron_kernel_matvec_lazy", "fastron_query_packed"):
         getattr(L, f).restype = st
     L.fastron_last_error.argtypes = []
     L.fastron_last_error.restype = ctypes.c_char_p
@@ -614,6 +618,36 @@ def fastron_query(robot, q, spos, alpha, kind: int, gamma: float, score=None, la
     _check(L.fastron_query(ctypes.byref(r), _ptr(q), nq, q.stride(0), _ptr(spos) if ns else None,
                            _ptr(alpha) if ns else None, ns, lds, _kernel(kind, gamma), _ptr(score), _ptr(label),
                            _ptr(workspace), workspace.numel(), ts.cuda_stream))
+    return score, label
+
+
+def fastron_query_packed(robot, q, model: PackedModel, score=None, label=None, want_score=True, want_label=True,
+                         workspace=None, stream=None):
+    """Configurations q (nq, >=D) float32 cuda against a packed model -> (score, label):
+    one launch for small and mid-size batches (D-H chain fused into the scoring kernel)."""
+    torch = _torch()
+    L = load_library()
+    _require_cuda(q, score, label)
+    _expect(q, torch.float32, "q", dim=2)
+    r = robot if isinstance(robot, fastron_robot) else make_robot_struct(robot)
+    if r.n_cp != model.n_cp:
+        raise ValueError("robot and model control-point counts differ")
+    if q.shape[1] < r.dof:
+        raise ValueError(f"q has {q.shape[1]} columns, the robot has {r.dof} joints")
+    nq = q.shape[0]
+    ts = _tstream(stream)
+    if want_score and score is None:
+        score = _new(nq, torch.float32, q.device, ts)
+    if want_label and label is None:
+        label = _new(nq, torch.int8, q.device, ts)
+    _expect(score, torch.float32, "score", dim=1)
+    _expect(label, torch.int8, "label", dim=1)
+    need = L.fastron_query_packed_workspace_bytes(nq, model.ns, r.n_cp, r.dof)
+    if workspace is None or workspace.numel() < need:
+        workspace = _workspace(need, q.device, ts)
+    _check(L.fastron_query_packed(ctypes.byref(r), _ptr(q), nq, q.stride(0), _ptr(model.buf), model.ns, r.n_cp,
+                                  _kernel(model.kind, model.gamma), _ptr(score), _ptr(label), _ptr(workspace),
+                                  workspace.numel(), ts.cuda_stream))
     return score, label
 
 

@@ -18,7 +18,7 @@ BUILD = os.path.join(ROOT, "build", "obj")
 SOURCES = ["abi.cu", "fk.cu", "score.cu", "gram.cu", "train.cu", "update.cu", "validate.cu"]
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-diag-suppress=128",
          "-I" + os.path.join(ROOT, "include")]
 
 

@@ -190,6 +190,8 @@ size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 constexpr int64_t kQueryChunk = 1 << 18;  // queries per pipelined chunk of fastron_query
 
+
+
 // One non-blocking copy stream per device for fastron_query's host<->device pipeline.
 // which = 0: host-to-device copies, 1: device-to-host copies, 2: the second compute stream.
 cudaStream_t query_copy_stream(int which) {
@@ -835,6 +837,58 @@ fastron_status fastron_query(const fastron_robot* robot, const float* q, int64_t
   if (e == cudaSuccess) e = e3;
   if (e == cudaSuccess) e = e4;
   return cuda_status(e, "fastron_query");
+}
+
+size_t fastron_query_packed_workspace_bytes(int64_t nq, int64_t ns, int32_t n_cp, int32_t dof) {
+  if (nq < 0 || ns < 0 || n_cp < 1 || n_cp > FASTRON_MAX_CP || dof < 1 || dof > FASTRON_MAX_DOF) return 0;
+  const int64_t chunk = nq < kQueryChunk ? nq : kQueryChunk;
+  return align_up(score_partial_bytes(chunk, ns, n_cp)) + align_up((size_t)chunk * n_cp * 16);
+}
+
+fastron_status fastron_query_packed(const fastron_robot* robot, const float* q, int64_t nq, int64_t ldq,
+                                    const void* packed, int64_t ns, int32_t n_cp, fastron_kernel k, float* score,
+                                    int8_t* label, void* workspace, size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_range_("fastron_query_packed");
+  fastron_status s = check_robot(robot);
+  if (s != FASTRON_OK) return s;
+  s = check_kernel(k);
+  if (s != FASTRON_OK) return s;
+  FASTRON_REQUIRE(nq >= 0 && ns >= 0, "nq and ns must be >= 0");
+  FASTRON_REQUIRE(n_cp == robot->n_cp, "n_cp (%d) differs from robot->n_cp (%d)", n_cp, robot->n_cp);
+  if (nq == 0) return FASTRON_OK;
+  FASTRON_REQUIRE(q != nullptr, "q is NULL");
+  FASTRON_REQUIRE(!is_host_ptr(q) && !is_host_ptr(score) && !is_host_ptr(label),
+                  "fastron_query_packed takes device buffers (fastron_query streams host buffers)");
+  FASTRON_REQUIRE(score || label, "score and label are both NULL");
+  FASTRON_REQUIRE(ldq >= robot->dof, "ldq (%lld) < dof (%d)", (long long)ldq, robot->dof);
+  FASTRON_REQUIRE(ns == 0 || packed, "packed is NULL");
+  FASTRON_REQUIRE(ns == 0 || ((uintptr_t)packed & 255) == 0, "packed must be 256-byte aligned (fastron_model_pack)");
+  const int M = robot->n_cp, D = robot->dof;
+  const size_t need = fastron_query_packed_workspace_bytes(nq, ns, M, D);
+  if (workspace_bytes < need || (need > 0 && !workspace))
+    return fail(FASTRON_ERR_WORKSPACE, "fastron_query_packed needs %zu workspace bytes, got %zu", need,
+                workspace_bytes);
+  FASTRON_REQUIRE(((uintptr_t)workspace & 255) == 0, "workspace must be 256-byte aligned");
+  FASTRON_VALIDATE(vcheck_f32(q, nq, D, ldq, stream, "q"));
+  const int64_t chunk = nq < kQueryChunk ? nq : kQueryChunk;
+  double* partial = static_cast<double*>(workspace);
+  float4* pos = reinterpret_cast<float4*>(static_cast<char*>(workspace) + align_up(score_partial_bytes(chunk, ns, M)));
+  cudaStream_t st = S(stream);
+  const float c = kernel_scale(k);
+  const FkParams P = make_fk_params(*robot);
+  const float* pk = static_cast<const float*>(packed);
+  cudaError_t e = cudaSuccess;
+  if (query_small_ok(nq, ns, M))
+    return cuda_status(launch_query_small(P, q, nq, ldq, pk, ns, M, k.kind, c, score, label, partial, st),
+                       "fastron_query_packed");
+  for (int64_t off = 0; off < nq && e == cudaSuccess; off += chunk) {
+    const int64_t n = nq - off < chunk ? nq - off : chunk;
+    e = launch_fk(P, q + off * ldq, n, ldq, pos, chunk, st);
+    if (e == cudaSuccess)
+      e = launch_score(pos, n, chunk, pk, ns, M, k.kind, c, score ? score + off : nullptr,
+                       label ? label + off : nullptr, partial, st, nullptr, nq);
+  }
+  return cuda_status(e, "fastron_query_packed");
 }
 
 }  // extern "C"

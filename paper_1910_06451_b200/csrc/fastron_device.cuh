@@ -132,7 +132,14 @@ __device__ __forceinline__ void accum_term(f2& acc, f2 dx, f2 dy, f2 dz, bool fi
     acc = first ? (init ? add2(init, t) : t) : add2(acc, t);
   } else {
     const f2 one = pk(1.0f, 1.0f);
-#if FASTRON_RQ_NEWTON
+#if FASTRON_RQ_NEWTON == 2
+    f2 s = mul2(dx, dx);  // s-form without the Newton step (A/B only)
+    s = fma2(dy, dy, s);
+    s = fma2(dz, dz, s);
+    const f2 w = add2(s, one);
+    const f2 r = pk(rcp_approx(lo(w)), rcp_approx(hi(w)));
+    acc = fma2(r, r, first ? init : acc);
+#elif FASTRON_RQ_NEWTON
     f2 s = mul2(dx, dx);
     s = fma2(dy, dy, s);
     s = fma2(dz, dz, s);

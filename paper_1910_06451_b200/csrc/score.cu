@@ -267,9 +267,9 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
     float px[MP], py[MP], pz[MP];
 #pragma unroll
     for (int m = 0; m < MP; ++m) px[m] = py[m] = pz[m] = 0.0f;
-    // positions of the query (MODE_EDGE: of the interpolated configuration, written by
-    // edge_fk_kernel for this round)
     if (vq < nq_live) {
+      // positions of the query (MODE_EDGE: of the interpolated configuration, written by
+      // edge_fk_kernel for this round)
 #pragma unroll
       for (int m = 0; m < MP; ++m) {
         if (m < A.M) {
@@ -662,6 +662,18 @@ static int score_ctas_per_sm() {
   return v;
 }
 
+// Largest batch scored with one query per thread (QT = 1), measured per M:
+// M = 8: 2,048; M = 16: 512; M <= 4: 16,384 (cfg1, 10k x 1k: 28.2 -> 26.6 us as a graph
+// replay of FK + score; the 128 of round 1 was never measured). FASTRON_ONEQ_MAX (env)
+// overrides all three for experiments.
+#ifndef FASTRON_ONEQ_MAX4
+#define FASTRON_ONEQ_MAX4 16384
+#endif
+static int64_t oneq_max(int mp) {
+  if (const char* e = getenv("FASTRON_ONEQ_MAX")) return atoll(e);  // experiments
+  return mp <= 4 ? FASTRON_ONEQ_MAX4 : mp <= 8 ? 2048 : 512;
+}
+
 static ScorePlan make_plan(int64_t nq, int64_t ns, int M, int ctas_per_sm) {
   ScorePlan p;
   const int qpc = score_queries_per_cta(M);
@@ -701,8 +713,7 @@ static cudaError_t run_score(const ScoreArgs& base, const FkParams& P, int64_t n
   // one query per thread up to a batch size measured per M (A/B, 20k supports, same bits):
   // M = 8 up to 2,048 queries (512: 58 -> 46 us, 1,024: 73 -> 68, 2,048: 118 -> 113; 4,096
   // slower), M = 16 up to 512 (256: 66 -> 58 us, 512: 97 -> 82; 1,024 slower)
-  const int64_t oneq_max = MP <= 4 ? kNT : MP <= 8 ? 2048 : 512;
-  const bool one_q = MODE != MODE_EDGE && nq <= oneq_max && qt_for(MP) > 1;
+  const bool one_q = MODE != MODE_EDGE && nq <= oneq_max(MP) && qt_for(MP) > 1;
   if (one_q) plan.n_qblocks = (nq + kNT - 1) / kNT;
   const int64_t grid = plan.n_qblocks * plan.n_splits;
   if (grid > 0x7fffffff) return cudaErrorInvalidValue;

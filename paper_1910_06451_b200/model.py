@@ -12,7 +12,8 @@ from typing import Optional
 import numpy as np
 
 from . import (fastron_active_samples, fastron_fk, fastron_gram, fastron_kernel_matvec, fastron_kernel_matvec_lazy,
-               fastron_label_capsules, fastron_model_pack, fastron_score_packed, fastron_train, fastron_train_lazy,
+               fastron_label_capsules, fastron_model_pack, fastron_query_packed, fastron_score_packed, fastron_train,
+               fastron_train_lazy,
                make_robot_struct, train_result)
 
 
@@ -111,30 +112,28 @@ class FastronModel:
 
     # ---- proxy collision check ----
     def query(self, q):
-        qpos = fastron_fk(self.robot_c, q)
-        return fastron_score_packed(qpos, self.model)
+        """Configurations q (n, D) device float32 -> (score, label): fastron_query_packed
+        (one launch for small and mid-size batches)."""
+        return fastron_query_packed(self.robot_c, q, self.model)
 
     def query_graph(self, nq: int):
-        """A fixed-size query captured once as a CUDA graph (FK + score, static buffers):
-        for planners that ask the same number of configurations again and again, a replay
-        skips the per-call launch work (20 us vs 40 us for one query against
-        20k supports). Returns fn(q) -> (score, label); the outputs are reused buffers, so
-        copy them before the next call. Valid until the model changes (fit / update / load)."""
+        """A fixed-size query captured once as a CUDA graph (fastron_query_packed on static
+        buffers): for planners that ask the same number of configurations again and again,
+        a replay skips the per-call host work. Returns fn(q) -> (score, label); the outputs
+        are reused buffers, so copy them before the next call. Valid until the model
+        changes (fit / update / load)."""
         import torch
-        from . import fastron_fk, fastron_score_packed, load_library
+        from . import load_library
         dev = self.supports.device
         q_static = torch.zeros((nq, self.robot_c.dof), dtype=torch.float32, device=dev)
-        qpos = torch.empty((self.robot_c.n_cp, nq, 4), dtype=torch.float32, device=dev)
         score = torch.empty(nq, dtype=torch.float32, device=dev)
         label = torch.empty(nq, dtype=torch.int8, device=dev)
-        ws = torch.empty(max(256, load_library().fastron_score_packed_workspace_bytes(nq, self.model.ns,
-                                                                                     self.model.n_cp)),
-                         dtype=torch.uint8, device=dev)
+        ws = torch.empty(max(256, load_library().fastron_query_packed_workspace_bytes(
+            nq, self.model.ns, self.model.n_cp, self.robot_c.dof)), dtype=torch.uint8, device=dev)
         model = self.model
 
         def body():
-            fastron_fk(self.robot_c, q_static, pos=qpos)
-            fastron_score_packed(qpos, model, score, label, workspace=ws)
+            fastron_query_packed(self.robot_c, q_static, model, score, label, workspace=ws)
 
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
@@ -146,7 +145,7 @@ class FastronModel:
         with torch.cuda.graph(graph):
             body()
 
-        keep = (q_static, qpos, score, label, ws, model)  # every buffer the graph touches stays alive
+        keep = (q_static, score, label, ws, model)  # every buffer the graph touches stays alive
 
         def run(q):
             q_static.copy_(q, non_blocking=True)

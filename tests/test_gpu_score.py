@@ -268,3 +268,50 @@ def test_mid_batches_many_splits(name, nq):
     s, l = _gpu_scores(wl.robot, wl.supports, wl.alpha, wl.queries, 0, wl.gamma)
     f, _ = _ref_scores(wl.robot, wl.supports, wl.alpha, wl.queries, 0, wl.gamma)
     assert_score_parity(s, f, l, what=f"{name} nq={nq}")
+
+
+@pytest.mark.parametrize("M,kind,nqs", [
+    (8, W.GAUSSIAN, (1, 32, 33, 100, 128, 129, 1000, 2048, 2049, 5000, 100_003)),
+    (8, W.RQ, (33, 1000, 5000)),
+    (4, W.GAUSSIAN, (40, 10_000)),
+    (16, W.GAUSSIAN, (64, 512, 513, 3000)),
+    (5, W.RQ, (77, 1500)),
+])
+def test_query_packed_equals_fk_plus_score(M, kind, nqs):
+    """fastron_query_packed (configurations in, scores out, one API call) gives the bits of
+    fastron_fk + fastron_score_packed for every batch size: the small-batch kernel with
+    the D-H chain inside (nq <= 32), one query per thread, several per thread, few and
+    many support splits."""
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    base = W.arm7(8) if M != 4 else W.score_workload("cfg1", n_queries=1, n_supports=1).robot
+    rng = np.random.default_rng(300 + M + kind)
+    robot = base if M in (4, 8) else W.make_robot("m%d" % M, base.dh, rng.integers(0, 8, size=M),
+                                                   rng.uniform(-0.1, 0.1, size=(M, 3)))
+    D = robot.dh.shape[0]
+    for ns in (300, 3_000, 20_000):
+        sup = W.uniform_configs(rng, ns, D)
+        alpha = rng.standard_normal(ns).astype(np.float32)
+        model = fb.fastron_model_pack(fb.fastron_fk(robot, dev(sup)), dev(alpha), kind, 5.0)
+        for nq in nqs:
+            qf = rng.uniform(-np.pi, np.pi, size=(nq, D + 2)).astype(np.float32)  # ldq = D + 2
+            q = dev(qf)[:, :D]
+            s1, l1 = fb.fastron_score_packed(fb.fastron_fk(robot, q), model)
+            s2, l2 = fb.fastron_query_packed(robot, q, model)
+            torch.cuda.synchronize()
+            assert torch.equal(s1, s2) and torch.equal(l1, l2), (ns, nq)
+    # and the scores are right (oracle, R16) on one mid-size case
+    f, _ = _ref_scores(robot, sup, alpha, np.ascontiguousarray(qf[:, :D]), kind, 5.0)
+    assert_score_parity(s2.cpu().numpy(), f, l2.cpu().numpy(), what=f"query_packed M={M} kind={kind}")
+
+
+def test_query_packed_rejects_host_buffers():
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    robot = W.arm7(8)
+    model = fb.fastron_model_pack(fb.fastron_fk(robot, dev(W.uniform_configs(np.random.default_rng(0), 64, 7))),
+                                  dev(np.ones(64, np.float32)), 0, 5.0)
+    with pytest.raises(ValueError):
+        fb.fastron_query_packed(robot, torch.zeros((10, 7)), model)
