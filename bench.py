@@ -317,7 +317,27 @@ def _time_rows(fb, torch, kind):
     nb = (n5 + 127) // 128
     rows["cfg5_gram"] = {"ms": ms, "n": n5, "mufu_frac": nb * (nb + 1) // 2 * 128 * 128 * 16 / (ms * 1e-3) / (148 * 16 * 1.965e9),
                          "write_GBps": n5 * n5 * 4 / ms * 1e-6}
+    # Algorithm 1 at cfg5 scale (N = 20,000, M = 16; labels by the moved cubes, R21): on the
+    # 1.6 GB Gram and with lazily computed columns (no Gram; the point planes of the 16
+    # slices exceed shared memory and live in L2) — the same run bit for bit
+    _, _, _, moved5 = W.cfg5_gram_workload()
+    P8 = np.transpose(fb.fastron_fk(tw.robot, torch.from_numpy(X5).cuda()).cpu().numpy()[:, :, :3], (1, 0, 2))
+    y5 = torch.from_numpy(W.capsule_aabb_labels(W.chain_points(P8.astype(np.float64)), moved5, 0.05)).cuda()
+    o5 = {}
+    ms = timed(lambda: o5.update(fb.fastron_train(K5, y5, 1.0, 20_000)), 2)
+    r5 = fb.train_result(o5["result"])
+    rows["cfg5_train"] = {"ms": ms, **r5, "us_per_iteration": ms * 1e3 / max(r5["iterations"], 1)}
     del K5
+    torch.cuda.empty_cache()
+    l5 = {}
+    lws5 = torch.empty(fb.load_library().fastron_train_lazy_workspace_bytes(n5, 16, 4096), dtype=torch.uint8,
+                       device="cuda")
+    ms = timed(lambda: l5.update(fb.fastron_train_lazy(pos5, y5, kind, 5.0, 1.0, 20_000, cache_cols=4096,
+                                                       workspace=lws5)), 2)
+    rl5 = fb.train_result(l5["result"])
+    rows["cfg5_train_lazy"] = {"ms": ms, **rl5, "us_per_iteration": ms * 1e3 / max(rl5["iterations"], 1),
+                               "same_as_full_gram": rl5 == r5 and bool(torch.equal(l5["alpha"], o5["alpha"]))}
+    del lws5
     torch.cuda.empty_cache()
     # the model-update cycle (Table I "update time" 55.8 ms incl. FCL labelling):
     # fit on cfg3, move 3 of the 6 cubes by 0.1 m (R21), then 2 draws near every support point +

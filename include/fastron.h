@@ -194,8 +194,10 @@ fastron_status fastron_train(const float* K, int64_t n, int64_t ldk, const int8_
  * fastron_train_lazy — Algorithm 1 with lazy kernel-matrix columns ("a column
  * of K can be computed and stored only when needed", :225 computeKernelMatrixColumn):
  * no Gram matrix is formed. The column of the selected index is computed inside the
- * persistent cluster kernel from the pre-scaled training points (held in shared memory)
- * and stored in a column cache of cache_cols columns; later steps on the same index
+ * persistent cluster kernel from the pre-scaled training points (held in shared memory,
+ * or — for slices beyond the shared-memory budget, e.g. n = 20,000 at n_cp = 16 — in an
+ * L2-resident part of the workspace) and stored in a column cache of cache_cols columns;
+ * later steps on the same index
  * read it back. Columns are bit-identical to fastron_gram's, so the result equals
  * fastron_train(fastron_gram(pos)) exactly.
  *   pos: device float4 [n_cp][ldp] control points of the n training configurations;
@@ -203,7 +205,8 @@ fastron_status fastron_train(const float* K, int64_t n, int64_t ldk, const int8_
  *   y, beta, iter_max, s_max, alpha_inout, F_inout, support_idx, trace, result: as
  *   fastron_train. cache_cols >= 0 (columns beyond the cache are recomputed).
  *   workspace: >= fastron_train_lazy_workspace_bytes(n, n_cp, cache_cols).
- * n <= fastron_train_lazy_max_n(n_cp), else FASTRON_ERR_UNSUPPORTED.
+ * n <= fastron_train_lazy_max_n(n_cp) (32,768: 16 CTAs x 2,048 slots), else
+ * FASTRON_ERR_UNSUPPORTED.
  */
 int64_t fastron_train_lazy_max_n(int32_t n_cp);
 size_t fastron_train_lazy_workspace_bytes(int64_t n, int32_t n_cp, int64_t cache_cols);

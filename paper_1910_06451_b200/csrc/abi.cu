@@ -424,7 +424,8 @@ int64_t fastron_train_lazy_max_n(int32_t n_cp) {
 
 size_t fastron_train_lazy_workspace_bytes(int64_t n, int32_t n_cp, int64_t cache_cols) {
   if (n < 0 || n_cp < 1 || n_cp > FASTRON_MAX_CP || cache_cols < 0) return 0;
-  return align_up(packed_bytes(n, n_cp)) + align_up((size_t)cache_cols * (size_t)n * 4);
+  return align_up(packed_bytes(n, n_cp)) + align_up((size_t)cache_cols * (size_t)n * 4) +
+         align_up(n_cp <= 16 ? train_lazy_plane_bytes(n, n_cp) : 0);
 }
 
 fastron_status fastron_train_lazy(const float* pos, int64_t n, int64_t ldp, int32_t n_cp, fastron_kernel k,
@@ -457,12 +458,13 @@ fastron_status fastron_train_lazy(const float* pos, int64_t n, int64_t ldp, int3
   char* ws = static_cast<char*>(workspace);
   float* packed = reinterpret_cast<float*>(ws);
   float* cache = reinterpret_cast<float*>(ws + align_up(packed_bytes(n, n_cp)));
+  void* planes = ws + align_up(packed_bytes(n, n_cp)) + align_up((size_t)cache_cols * (size_t)n * 4);
   cudaStream_t st = S(stream);
   cudaError_t e =
       launch_pack(reinterpret_cast<const float4*>(pos), ldp, nullptr, n, n_cp, kernel_scale(k), packed, st);
   if (e == cudaSuccess)
     e = launch_train_lazy(packed, n, n_cp, k.kind, y, beta, iter_max, s_max, alpha_inout, F_inout, support_idx, trace,
-                          result, cache, cache_cols, st);
+                          result, cache, cache_cols, planes, st);
   return cuda_status(e, "fastron_train_lazy");
 }
 

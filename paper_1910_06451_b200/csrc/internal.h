@@ -113,8 +113,10 @@ cudaError_t launch_train(const float* K, int64_t n, int64_t ldk, const int8_t* y
                          int64_t s_max, double* alpha, double* F, int32_t* support_idx, int32_t* trace, void* result,
                          cudaStream_t st);
 int64_t train_lazy_max_n(int M);
+size_t train_lazy_plane_bytes(int64_t n, int M);  // global point planes needed (0: shared memory)
 cudaError_t launch_train_lazy(const float* packed, int64_t n, int M, int kind, const int8_t* y, double beta,
                               int64_t iter_max, int64_t s_max, double* alpha, double* F, int32_t* support_idx,
-                              int32_t* trace, void* result, float* cache, int64_t cache_cols, cudaStream_t st);
+                              int32_t* trace, void* result, float* cache, int64_t cache_cols, void* planes,
+                              cudaStream_t st);
 
 }  // namespace fastron

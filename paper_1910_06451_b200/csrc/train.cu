@@ -99,6 +99,7 @@ struct TrainArgs {
   // lazy-column mode: K columns computed on demand and cached
   const float* packed;   // pre-scaled training points in the scoring tile layout
   float* cache;          // [cache_cols][n]
+  f2* gpts;              // GPTS instances: the point planes in global memory (L2), per rank
   int64_t cache_cols;
   int32_t M, m_pow2;
   float inv_m;
@@ -273,7 +274,10 @@ __device__ __forceinline__ Decision decide_removal(Decision d, const Cand& b, in
 
 // LMP = 0: K is given (fastron_train). LMP > 0: lazy columns of the FK kernel with LMP
 // padded control points and term LKIND (fastron_train_lazy).
-template <int EPT, int LMP, int LKIND>
+// GPTS: the lazy mode's point planes live in global memory (L2-resident scratch from the
+// workspace) instead of shared memory — slices too large for the 200 KB budget (N = 20,000
+// at M = 16: 1,250 points x 192 B per CTA). A computed column then reads its planes from L2.
+template <int EPT, int LMP, int LKIND, bool GPTS = false>
 __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constant__ TrainArgs A) {
   constexpr bool LAZY = LMP > 0;
   constexpr int LNP = LAZY ? LMP / 2 : 1;
@@ -290,8 +294,10 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
   // its own points, so consecutive lanes read consecutive 8-byte words — conflict-free
   // (a per-point record layout put every lane on the same banks: 32-way conflicts, ~11k
   // cycles per computed column). Then the cache slot of each local index's K column.
-  f2* s_pts = reinterpret_cast<f2*>(smem_raw + ((A.chunk * 8 + 15) & ~15ll));
-  int32_t* s_slot = reinterpret_cast<int32_t*>(s_pts + (LAZY ? A.chunk * LNP * 3 : 0));
+  f2* s_pts = GPTS ? A.gpts + (int64_t)rank * LNP * 3 * A.chunk
+                   : reinterpret_cast<f2*>(smem_raw + ((A.chunk * 8 + 15) & ~15ll));
+  int32_t* s_slot = GPTS ? reinterpret_cast<int32_t*>(smem_raw + ((A.chunk * 8 + 15) & ~15ll))
+                         : reinterpret_cast<int32_t*>(s_pts + (LAZY ? A.chunk * LNP * 3 : 0));
   __shared__ Cand s_warp[2][kTrainWarps];
   __shared__ CandBox s_inbox[2][kMaxCluster];               // C > 1: the CTA winners of an exchange
   __shared__ __align__(8) uint64_t s_inbar[2];              // their arrival barriers
@@ -355,6 +361,16 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
   int64_t nnz = 0;
   for (int r = 0; r < C; ++r) nnz += *cluster.map_shared_rank(&s_cta_cnt[0], r);
 
+  // loop invariants: clamped K-row offsets of the slots and the label sign bit of each
+  // slot as an fp64 high-word mask (y_j fl(d K) is fl(d K) with its sign flipped)
+  int koff[EPT];
+  uint32_t sgn[EPT];
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    koff[k] = min(k * kTrainNT + tid, jlast);
+    sgn[k] = ((yneg >> k) & 1u) << 31;
+  }
+
   // C > 1: exchange number ex uses inbox slot ex & 1 at barrier phase (ex >> 1) & 1. A peer
   // cannot send into a slot again before this CTA has consumed it: its next message there
   // needs this CTA's message of the exchange in between, sent only after this CTA's
@@ -375,19 +391,10 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
     }
     mbar_wait_cluster(&s_inbar[b], (ex >> 1) & 1u);
     ++ex;
+
     return for_max ? warp_best<true>(lane < C ? s_inbox[b][lane].c : cand_none(true))
                    : warp_best<false>(lane < C ? s_inbox[b][lane].c : cand_none(false));
   };
-
-  // loop invariants: clamped K-row offsets of the slots and the label sign bit of each
-  // slot as an fp64 high-word mask (y_j fl(d K) is fl(d K) with its sign flipped)
-  int koff[EPT];
-  uint32_t sgn[EPT];
-#pragma unroll
-  for (int k = 0; k < EPT; ++k) {
-    koff[k] = min(k * kTrainNT + tid, jlast);
-    sgn[k] = ((yneg >> k) & 1u) << 31;
-  }
 
   int64_t iters = 0, n_add = 0, n_remove = 0;
   int upd_i = -1;  // row of the pending rank-one update of F
@@ -680,13 +687,13 @@ static int train_cluster_size(int64_t n, int64_t chunk_max) {
   return (int)C;
 }
 
-template <int EPT, int LMP = 0, int LKIND = 0>
+template <int EPT, int LMP = 0, int LKIND = 0, bool GPTS = false>
 static cudaError_t launch_ept(const TrainArgs& A, int C, cudaStream_t st, size_t smem) {
   static std::atomic<int> attr[kMaxDevices];
   const int dev = device_slot();
   if (!attr[dev].load()) {
-    cudaFuncSetAttribute(train_kernel<EPT, LMP, LKIND>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(train_kernel<EPT, LMP, LKIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(train_kernel<EPT, LMP, LKIND, GPTS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(train_kernel<EPT, LMP, LKIND, GPTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr[dev].store(1);
   }
   cudaLaunchConfig_t cfg = {};
@@ -701,7 +708,7 @@ static cudaError_t launch_ept(const TrainArgs& A, int C, cudaStream_t st, size_t
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, train_kernel<EPT, LMP, LKIND>, A);
+  return cudaLaunchKernelEx(&cfg, train_kernel<EPT, LMP, LKIND, GPTS>, A);
 }
 
 cudaError_t launch_train(const float* K, int64_t n, int64_t ldk, const int8_t* y, double beta, int64_t iter_max,
@@ -725,6 +732,7 @@ cudaError_t launch_train(const float* K, int64_t n, int64_t ldk, const int8_t* y
   A.chunk = (n + C - 1) / C;
   if (A.chunk < 1) A.chunk = 1;
   A.packed = nullptr;
+  A.gpts = nullptr;
   A.cache = nullptr;
   A.cache_cols = 0;
   A.M = 1;
@@ -752,16 +760,37 @@ constexpr int kLazyMaxEPT = 8;             // slots per thread in the lazy mode
 
 static int64_t lazy_bytes_per_slot(int MP) { return 8 + 4 + (int64_t)(MP / 2) * 24; }
 
-int64_t train_lazy_max_n(int M) {
-  const int MP = padded_m(M);
+// slices up to this many points keep their planes in shared memory; larger ones (up to
+// kLazyMaxEPT x 256 per CTA) use the GPTS instance with the planes in global memory
+static int64_t lazy_smem_chunk(int MP) {
   int64_t chunk = kLazySmem / lazy_bytes_per_slot(MP);
-  if (chunk > kLazyMaxEPT * kTrainNT) chunk = kLazyMaxEPT * kTrainNT;
-  return chunk * kMaxCluster;
+  return chunk > kLazyMaxEPT * kTrainNT ? kLazyMaxEPT * kTrainNT : chunk;
+}
+
+int64_t train_lazy_max_n(int M) {
+  (void)M;
+  return (int64_t)kLazyMaxEPT * kTrainNT * kMaxCluster;
+}
+
+// FASTRON_LAZY_GPTS=1 (env, tests): global point planes even where shared memory suffices
+static bool lazy_force_gpts() {
+  const char* e = getenv("FASTRON_LAZY_GPTS");
+  return e && e[0] == '1';
+}
+
+// bytes of global point planes fastron_train_lazy needs for n points (0: shared memory)
+size_t train_lazy_plane_bytes(int64_t n, int M) {
+  const int MP = padded_m(M);
+  if (train_cluster_size(n, lazy_smem_chunk(MP)) <= kMaxCluster && !lazy_force_gpts()) return 0;
+  const int C = train_cluster_size(n, (int64_t)kLazyMaxEPT * kTrainNT);
+  const int64_t chunk = (n + C - 1) / C;
+  return (size_t)C * chunk * (MP / 2) * 3 * sizeof(f2);
 }
 
 template <int MP, int KIND>
 static cudaError_t launch_lazy_mp(const TrainArgs& A, int C, cudaStream_t st, size_t smem) {
   const int64_t ept = (A.chunk + kTrainNT - 1) / kTrainNT;
+  if (A.gpts) return launch_ept<kLazyMaxEPT, MP, KIND, true>(A, C, st, smem);
   if (ept <= 2) return launch_ept<2, MP, KIND>(A, C, st, smem);
   if (ept <= 4) return launch_ept<4, MP, KIND>(A, C, st, smem);
   return launch_ept<kLazyMaxEPT, MP, KIND>(A, C, st, smem);
@@ -769,12 +798,13 @@ static cudaError_t launch_lazy_mp(const TrainArgs& A, int C, cudaStream_t st, si
 
 cudaError_t launch_train_lazy(const float* packed, int64_t n, int M, int kind, const int8_t* y, double beta,
                               int64_t iter_max, int64_t s_max, double* alpha, double* F, int32_t* support_idx,
-                              int32_t* trace, void* result, float* cache, int64_t cache_cols, cudaStream_t st) {
+                              int32_t* trace, void* result, float* cache, int64_t cache_cols, void* planes,
+                              cudaStream_t st) {
   const int MP = padded_m(M);
-  int64_t chunk_max = kLazySmem / lazy_bytes_per_slot(MP);
-  if (chunk_max > kLazyMaxEPT * kTrainNT) chunk_max = kLazyMaxEPT * kTrainNT;
-  const int C = train_cluster_size(n, chunk_max);  // as in launch_train (lazy cfg3: C = 5)
-  if (C > kMaxCluster) return cudaErrorInvalidValue;
+  int C = train_cluster_size(n, lazy_smem_chunk(MP));  // as in launch_train (lazy cfg3: C = 5)
+  const bool gpts = C > kMaxCluster || lazy_force_gpts();
+  if (gpts) C = train_cluster_size(n, (int64_t)kLazyMaxEPT * kTrainNT);
+  if (C > kMaxCluster || (gpts && !planes)) return cudaErrorInvalidValue;
   TrainArgs A;
   A.K = nullptr;
   A.n = n;
@@ -791,12 +821,14 @@ cudaError_t launch_train_lazy(const float* packed, int64_t n, int M, int kind, c
   A.chunk = (n + C - 1) / C;
   if (A.chunk < 1) A.chunk = 1;
   A.packed = packed;
+  A.gpts = gpts ? static_cast<f2*>(planes) : nullptr;
   A.cache = cache;
   A.cache_cols = cache_cols;
   A.M = M;
   A.m_pow2 = (M & (M - 1)) == 0;
   A.inv_m = 1.0f / (float)M;
-  const size_t smem = (size_t)((A.chunk * 8 + 15) & ~15ll) + (size_t)A.chunk * (MP / 2) * 24 + (size_t)A.chunk * 4;
+  const size_t smem = (size_t)((A.chunk * 8 + 15) & ~15ll) + (gpts ? 0 : (size_t)A.chunk * (MP / 2) * 24) +
+                      (size_t)A.chunk * 4;
   cudaError_t e;
   switch (MP) {
 #define FASTRON_LCASE(mp)                                                                              \

@@ -264,3 +264,34 @@ def test_train_every_cluster_size_same_run():
             os.environ.pop("FASTRON_TRAIN_CLUSTER", None)
         else:
             os.environ["FASTRON_TRAIN_CLUSTER"] = old
+
+
+def test_train_removals_on_cluster():
+    """Algorithm 1's removal branch (max over alpha != 0 of y(F - alpha) > 0)
+    on the cluster path (N = 2,500 > 2,048: C = 3 by default, and forced C = 2 and 8): a
+    cold run and a warm start after label flips at gamma = 20, where the
+    runs converge and remove supports, must retrace the oracle exactly, n_remove > 0."""
+    require_gpu()
+    wl = W.train_workload(2500)
+    y = _labels(wl)
+    _, K = _gram(wl.robot, wl.X, 0, 20.0)
+    K64 = K.cpu().numpy().astype(np.float64)
+    first = oracle.train(K64, y, 1.0, 20_000)
+    y2 = y.copy()
+    y2[::7] *= -1
+    warm = oracle.train(K64, y2, 1.0, 20_000, alpha0=first["alpha"], F0=first["F"])
+    assert first["n_remove"] > 0 and warm["n_remove"] > 0 and warm["converged"]
+    old = os.environ.get("FASTRON_TRAIN_CLUSTER")
+    try:
+        for C in (None, 2, 8):
+            if C is None:
+                os.environ.pop("FASTRON_TRAIN_CLUSTER", None)
+            else:
+                os.environ["FASTRON_TRAIN_CLUSTER"] = str(C)
+            _assert_same_run(_gpu_train(K, y, 1.0, 20_000), first)
+            _assert_same_run(_gpu_train(K, y2, 1.0, 20_000, alpha0=first["alpha"], F0=first["F"]), warm)
+    finally:
+        if old is None:
+            os.environ.pop("FASTRON_TRAIN_CLUSTER", None)
+        else:
+            os.environ["FASTRON_TRAIN_CLUSTER"] = old

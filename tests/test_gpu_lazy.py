@@ -88,3 +88,64 @@ def test_lazy_odd_m_equals_full_gram(M):
     assert fb.train_result(full["result"]) == fb.train_result(lazy["result"])
     assert np.array_equal(full["alpha"].cpu().numpy(), lazy["alpha"].cpu().numpy())
     assert np.array_equal(full["F"].cpu().numpy(), lazy["F"].cpu().numpy())
+
+
+def _same(full, lazy):
+    import paper_1910_06451_b200 as fb
+    rf, rl = fb.train_result(full["result"]), fb.train_result(lazy["result"])
+    assert rf == rl
+    it = rf["iterations"]
+    assert np.array_equal(full["trace"].cpu().numpy()[:it], lazy["trace"].cpu().numpy()[:it])
+    assert np.array_equal(full["alpha"].cpu().numpy(), lazy["alpha"].cpu().numpy())
+    assert np.array_equal(full["F"].cpu().numpy(), lazy["F"].cpu().numpy())
+    ns = rf["n_support"]
+    assert np.array_equal(full["support_idx"].cpu().numpy()[:ns], lazy["support_idx"].cpu().numpy()[:ns])
+    return rf
+
+
+def test_lazy_cfg5_scale_equals_full_gram():
+    """f1 at cfg5 scale (N = 20,000, M = 16): the 16-CTA slices of
+    1,250 points exceed the shared-memory budget, so the point planes live in an
+    L2-resident part of the workspace; the run must equal fastron_train(fastron_gram(pos))
+    bit for bit — without the 1.6 GB Gram."""
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    robot, X, _, moved = W.cfg5_gram_workload()
+    assert X.shape[0] == 20_000 and robot.n_cp == 16
+    assert fb.load_library().fastron_train_lazy_max_n(16) >= 20_000
+    y = W.capsule_aabb_labels(W.chain_points(oracle.fk(W.arm7(8), X)), moved, 0.05)
+    pos = fb.fastron_fk(robot, dev(X))
+    yd = dev(y)
+    lazy = fb.fastron_train_lazy(pos, yd, 0, 5.0, 1.0, 20_000, cache_cols=4096)
+    K = fb.fastron_gram(pos, 0, 5.0)
+    full = fb.fastron_train(K, yd, 1.0, 20_000)
+    torch.cuda.synchronize()
+    del K
+    rf = _same(full, lazy)
+    assert rf["iterations"] > 1000
+
+
+def test_lazy_global_planes_forced(tmp_path):
+    """The global-plane instance (FASTRON_LAZY_GPTS=1, read per call) on small problems:
+    odd M, RQ, a tiny cache, a warm start — equal to the shared-memory lazy run and so to
+    the full-Gram run."""
+    require_gpu()
+    import os
+    import torch
+    import paper_1910_06451_b200 as fb
+    wl = W.train_workload(1700)
+    rng = np.random.default_rng(5)
+    robot = W.make_robot("m5", wl.robot.dh, rng.integers(1, 8, size=5), rng.uniform(-0.1, 0.1, size=(5, 3)))
+    y = W.capsule_aabb_labels(W.chain_points(oracle.fk(wl.robot, wl.X)), wl.cubes, wl.radius)
+    pos = fb.fastron_fk(robot, dev(wl.X))
+    yd = dev(y)
+    for kind, cache in ((0, 4096), (1, 13)):
+        ref = fb.fastron_train_lazy(pos, yd, kind, wl.gamma, 1.0, 3000, cache_cols=cache)
+        os.environ["FASTRON_LAZY_GPTS"] = "1"
+        try:
+            got = fb.fastron_train_lazy(pos, yd, kind, wl.gamma, 1.0, 3000, cache_cols=cache)
+        finally:
+            os.environ.pop("FASTRON_LAZY_GPTS", None)
+        torch.cuda.synchronize()
+        _same(ref, got)
