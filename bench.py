@@ -45,6 +45,26 @@ def _peaks():
         return {}
 
 
+def _parity(kind: int):
+    """The committed parity statistics of this workload (tests/tools/parity_report.py, which
+    compares the GPU path with oracle/ under SURVEY §8(c) C4; bench.py only reads its file)."""
+    path = os.path.join(ROOT, "profiles", "r02", "parity.json")
+    try:
+        with open(path) as f:
+            rep = json.load(f)
+    except Exception:
+        return None
+    k = "gaussian" if kind == 0 else "rq"
+    keep = ("checked", "sample", "max_err", "p9999_err", "rms_err", "violations", "max_err_over_tol",
+            "near_zero", "near_zero_max_err", "label_mismatches")
+    out = {"source": "profiles/r02/parity.json", "tolerance": "max(1e-4 |f|, 1e-5); labels where |f_ref| > 1e-4"}
+    for name in ("headline", "cfg2", "cfg5", "cfg1"):
+        st = rep.get(f"{name}_{k}")
+        if st:
+            out[name] = {kk: st[kk] for kk in keep if kk in st}
+    return out
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -436,7 +456,9 @@ def _time_rows(fb, torch, kind):
     evaluated = int(np.sum(rounds * 32))
     rows["cfg4_edges"] = {"ms": ms, "edges_per_s": len(ew.qa) / ms * 1e3, "in_collision_fraction": float(hit.mean()),
                           "configs_evaluated": evaluated,
-                          "evaluated_kernel_evals_per_s": evaluated * len(ew.supports) / ms * 1e3}
+                          "evaluated_kernel_evals_per_s": evaluated * len(ew.supports) / ms * 1e3,
+                          "mufu_frac_evaluated": evaluated * len(ew.supports) * ew.robot.n_cp / (ms * 1e-3)
+                          / (148 * 16 * 1.965e9)}
     return rows
 
 
@@ -450,9 +472,13 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     fb.load_library()
     wl = W.score_workload("headline", kind=args.kind)
-    Q, S, M = len(wl.queries), len(wl.supports), wl.robot.n_cp
     from paper_1910_06451_b200 import dist as fd
-    queries = fd.shard_queries(wl.queries, rank)  # weak scaling: every rank its own batch
+    if args.strong:  # strong scaling: the one 1M-query batch cut into contiguous shards
+        queries = np.ascontiguousarray(fd.shard(wl.queries, rank, ws))
+    else:  # weak scaling: every rank its own batch of the workload's size
+        queries = fd.shard_queries(wl.queries, rank)
+    Q_total = len(wl.queries) if args.strong else ws * len(wl.queries)
+    Q, S, M = len(queries), len(wl.supports), wl.robot.n_cp
     robot = fb.make_robot_struct(wl.robot)
     st = torch.cuda.current_stream()
 
@@ -506,7 +532,7 @@ def run_ours(args):
     sc_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
     step_each = np.array([e[0].elapsed_time(e[2]) for e in ev])  # per-step FK start -> score end
     ms_step = fd.max_over_ranks(ms_total / args.steps, device="cuda")
-    value = fd.aggregate_rate(Q, ws, ms_step)
+    value = Q_total / (ms_step * 1e-3)  # all ranks' queries / the slowest rank's time
     clocks = clk.summary()
 
     # ---- end to end through the public API with host buffers (pinned), rank-local ----
@@ -531,6 +557,32 @@ def run_ours(args):
     e1.synchronize()
     e2e_ms = fd.max_over_ranks(e0.elapsed_time(e1) / args.steps, device="cuda")
     assert np.array_equal(sh.numpy(), score.cpu().numpy()), "fastron_query disagrees with fk + score_packed"
+
+    # ---- sharded edge checks (cfg4, strong scaling): the 10k edges cut into contiguous
+    #      shards, each rank checks its shard against the broadcast packed model ----
+    ew = W.edge_workload(kind=args.kind)
+    emodel = fb.fastron_model_pack(fb.fastron_fk(robot, torch.from_numpy(ew.supports).cuda()),
+                                   torch.from_numpy(ew.alpha).cuda(), ew.kind, ew.gamma)
+    if ws > 1:
+        fd.broadcast_model(emodel.buf, src=0)
+    eqa, eqb = torch.from_numpy(ew.qa).cuda(), torch.from_numpy(ew.qb).cuda()
+    eshard = lambda a, b: fb.fastron_edge_check_packed(robot, a, b, ew.n_interp, emodel)
+    for _ in range(args.warmup):
+        fd.sharded_map(eshard, len(ew.qa), eqa, eqb, gather=False)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ee0.record(st)
+    for _ in range(args.steps):
+        fd.sharded_map(eshard, len(ew.qa), eqa, eqb, gather=False)
+    ee1.record(st)
+    ee1.synchronize()
+    edge_ms = fd.max_over_ranks(ee0.elapsed_time(ee1) / args.steps, device="cuda")
+    hit_all = fd.sharded_map(eshard, len(ew.qa), eqa, eqb)[0]  # gathered in edge order on every rank
+    edges = {"workload": "cfg4 (10k edges x 64 points, 3k supports)", "scaling": "strong",
+             "edges_per_s": len(ew.qa) / (edge_ms * 1e-3), "ms": edge_ms, "edges_per_gpu": len(fd.shard(ew.qa, rank, ws)),
+             "in_collision_fraction": float(hit_all.float().mean().item())}
 
     # ---- roofline of the dominant kernel (the score launch) ----
     peaks = _peaks()
@@ -566,22 +618,26 @@ def run_ours(args):
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "strong" if args.strong else "weak",
                 "vs_baseline": None, "dtype": "f32 (fp64 FK and accumulation)", "data": "synthetic",
-                "config": {"workload": "headline", "model": "cfg2 7-DOF arm, M=8", "global_batch": ws * Q,
+                "config": {"workload": "headline", "model": "cfg2 7-DOF arm, M=8", "global_batch": Q_total,
                            "queries_per_gpu": Q, "n_supports": S, "n_cp": M, "dof": wl.robot.dof,
                            "gamma": wl.gamma, "kernel": "gaussian" if wl.kind == 0 else "rq",
-                           "parallelism": f"dp{ws} (query shards, replicated model)",
+                           "parallelism": f"dp{ws} ({'contiguous shards of one batch' if args.strong else 'a batch per rank'}"
+                                          ", replicated model)",
                            "l2": "inputs larger than L2 (28 MB queries + 128 MB positions per step > 126 MB)"},
                 "kernel_evals_per_s": value * S,
                 "step_ms": {"min": float(step_each.min()), "median": float(np.median(step_each)),
                             "max": float(step_each.max())},
                 "roofline": roof,
                 "cpu_baseline": base,
-                "e2e": {"value": fd.aggregate_rate(Q, ws, e2e_ms), "unit": UNIT, "h2d_bytes_per_step": Q * wl.robot.dof * 4,
+                "e2e": {"value": Q_total / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": Q * wl.robot.dof * 4,
                         "d2h_bytes_per_step": Q * 5, "ms_per_step": e2e_ms,
                         "api": "fastron_query with pinned host q/score/label"},
                 "gpu_launches": launches,
+                "edge_check": edges,
+                "parity": _parity(args.kind),
                 "clocks": clocks}
         if rows is not None:
             line["rows"] = rows
@@ -600,6 +656,8 @@ def main():
     ap.add_argument("--kind", type=int, default=0, help="0 = Gaussian (north star), 1 = RQ (PAPER.md Eq. 3)")
     ap.add_argument("--rows", action="store_true", help="also time cfg1/cfg2/cfg3/cfg4 rows")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: split the one 1M-query batch over the ranks (default: weak, 1M per rank)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # `python bench.py --gpus N` without a launcher: start one rank per GPU ourselves,

@@ -265,6 +265,16 @@ fastron_status fastron_kernel_matvec_lazy(const float* pos, int64_t n, int64_t l
  *   workspace: >= fastron_edge_workspace_bytes(n_edges, ns, robot->n_cp).
  */
 size_t fastron_edge_workspace_bytes(int64_t n_edges, int64_t ns, int32_t n_cp);
+/* fastron_edge_check_packed — the same check against a model packed once by
+ * fastron_model_pack (e.g. replicated to every GPU by one broadcast of the packed buffer,
+ * DESIGN.md §8): the same rounds, the same results. packed: device, 256-byte aligned;
+ * n_cp == robot->n_cp. workspace (256-byte aligned):
+ * >= fastron_edge_packed_workspace_bytes(n_edges, ns, n_cp). */
+size_t fastron_edge_packed_workspace_bytes(int64_t n_edges, int64_t ns, int32_t n_cp);
+fastron_status fastron_edge_check_packed(const fastron_robot* robot, const float* qa, const float* qb,
+                                         int64_t n_edges, int64_t ldq, int32_t n_interp, const void* packed,
+                                         int64_t ns, int32_t n_cp, fastron_kernel k, uint8_t* in_collision,
+                                         int32_t* hit_index, void* workspace, size_t workspace_bytes, void* stream);
 fastron_status fastron_edge_check(const fastron_robot* robot, const float* qa, const float* qb, int64_t n_edges,
                                   int64_t ldq, int32_t n_interp, const float* spos, const float* alpha, int64_t ns,
                                   int64_t lds, fastron_kernel k, uint8_t* in_collision, int32_t* hit_index,

@@ -35,6 +35,7 @@ EXPORTED = [
     "fastron_kernel_matvec", "fastron_score_packed_f64", "fastron_set_validation", "fastron_validation",
     "fastron_kernel_matvec_lazy_workspace_bytes", "fastron_kernel_matvec_lazy",
     "fastron_query_packed_workspace_bytes", "fastron_query_packed",
+    "fastron_edge_packed_workspace_bytes", "fastron_edge_check_packed",
 ]
 
 
@@ -117,6 +118,10 @@ def load_library(path: str = LIB_PATH):
     L.fastron_edge_workspace_bytes.argtypes = [i64, i64, i32]
     L.fastron_edge_workspace_bytes.restype = sz
     L.fastron_edge_check.argtypes = [rp, vp, vp, i64, i64, i32, vp, vp, i64, i64, fastron_kernel, vp, vp, vp, sz, vp]
+    L.fastron_edge_packed_workspace_bytes.argtypes = [i64, i64, i32]
+    L.fastron_edge_packed_workspace_bytes.restype = sz
+    L.fastron_edge_check_packed.argtypes = [rp, vp, vp, i64, i64, i32, vp, i64, i32, fastron_kernel, vp, vp, vp, sz,
+                                            vp]
     L.fastron_query_workspace_bytes.argtypes = [i64, i64, i32, i32]
     L.fastron_query_workspace_bytes.restype = sz
     L.fastron_query.argtypes = [rp, vp, i64, i64, vp, vp, i64, i64, fastron_kernel, vp, vp, vp, sz, vp]
@@ -126,7 +131,7 @@ def load_library(path: str = LIB_PATH):
     for f in ("fastron_fk", "fastron_score", "fastron_gram", "fastron_train", "fastron_edge_check", "fastron_query",
               "fastron_model_pack", "fastron_score_packed", "fastron_score_joint", "fastron_gram_joint", "fastron_train_lazy", "fastron_active_samples",
               "fastron_label_capsules", "fastron_kernel_matvec", "fastron_score_packed_f64",
-              "fastron_kernel_matvec_lazy", "fastron_query_packed"):
+              "fastron_kernel_matvec_lazy", "fastron_query_packed", "fastron_edge_check_packed"):
         getattr(L, f).restype = st
     L.fastron_last_error.argtypes = []
     L.fastron_last_error.restype = ctypes.c_char_p
@@ -593,6 +598,37 @@ def fastron_edge_check(robot, qa, qb, n_interp: int, spos, alpha, kind: int, gam
                                 _ptr(spos) if ns else None, _ptr(alpha) if ns else None, ns, lds, _kernel(kind, gamma),
                                 _ptr(in_collision), _ptr(hit_index), _ptr(workspace), workspace.numel(),
                                 ts.cuda_stream))
+    return in_collision, hit_index
+
+
+def fastron_edge_check_packed(robot, qa, qb, n_interp: int, model: PackedModel, in_collision=None, hit_index=None,
+                              want_hit_index=True, workspace=None, stream=None):
+    """fastron_edge_check against a packed (e.g. broadcast) model."""
+    torch = _torch()
+    L = load_library()
+    _require_cuda(qa, qb, in_collision, hit_index)
+    _expect(qa, torch.float32, "qa", dim=2)
+    _expect(qb, torch.float32, "qb", dim=2)
+    r = robot if isinstance(robot, fastron_robot) else make_robot_struct(robot)
+    if r.n_cp != model.n_cp:
+        raise ValueError("robot and model control-point counts differ")
+    E = qa.shape[0]
+    if qa.shape != qb.shape or qa.stride(0) != qb.stride(0):
+        raise ValueError("qa and qb must have the same shape and leading dimension")
+    ts = _tstream(stream)
+    if in_collision is None:
+        in_collision = _new(E, torch.uint8, qa.device, ts)
+    if want_hit_index and hit_index is None:
+        hit_index = _new(E, torch.int32, qa.device, ts)
+    _expect(in_collision, torch.uint8, "in_collision", dim=1)
+    _expect(hit_index, torch.int32, "hit_index", dim=1)
+    need = L.fastron_edge_packed_workspace_bytes(E, model.ns, r.n_cp)
+    if workspace is None or workspace.numel() < need:
+        workspace = _workspace(need, qa.device, ts)
+    _check(L.fastron_edge_check_packed(ctypes.byref(r), _ptr(qa), _ptr(qb), E, qa.stride(0), int(n_interp),
+                                       _ptr(model.buf), model.ns, r.n_cp, _kernel(model.kind, model.gamma),
+                                       _ptr(in_collision), _ptr(hit_index), _ptr(workspace), workspace.numel(),
+                                       ts.cuda_stream))
     return in_collision, hit_index
 
 

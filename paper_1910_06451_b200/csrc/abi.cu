@@ -23,22 +23,25 @@ namespace fastron {
 
 std::atomic<int64_t> g_launches{0};
 
+// Per-device properties, queried once. The fast path is a lock-free acquire load of the
+// device's ready flag (the mutex only serialises the first query per device).
 const DeviceInfo& device_info() {
   static DeviceInfo infos[64];
-  static bool ready[64] = {};
+  static std::atomic<bool> ready[64] = {};
   static std::mutex mu;
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) dev = 0;
+  if (ready[dev].load(std::memory_order_acquire)) return infos[dev];
   std::lock_guard<std::mutex> g(mu);
-  if (!ready[dev]) {
+  if (!ready[dev].load(std::memory_order_relaxed)) {
     cudaDeviceProp p;
     if (cudaGetDeviceProperties(&p, dev) == cudaSuccess) {
       infos[dev] = DeviceInfo{dev, p.multiProcessorCount, (int)p.sharedMemPerBlockOptin};
     } else {
       infos[dev] = DeviceInfo{dev, 148, 227 * 1024};
     }
-    ready[dev] = true;
+    ready[dev].store(true, std::memory_order_release);
   }
   return infos[dev];
 }
@@ -539,18 +542,61 @@ fastron_status fastron_kernel_matvec_lazy(const float* pos, int64_t n, int64_t l
   return cuda_status(e, "fastron_kernel_matvec_lazy");
 }
 
-size_t fastron_edge_workspace_bytes(int64_t n_edges, int64_t ns, int32_t n_cp) {
+size_t fastron_edge_packed_workspace_bytes(int64_t n_edges, int64_t ns, int32_t n_cp) {
   if (n_edges < 0 || ns < 0 || n_cp < 1 || n_cp > FASTRON_MAX_CP) return 0;
   const size_t lists = 2 * align_up((size_t)n_edges * 4) + 256;  // two active lists + two counters
   const size_t pos = align_up((size_t)n_edges * 32 * n_cp * 16);  // a round's control points
-  return align_up(packed_bytes(ns, n_cp)) + align_up(score_partial_bytes(n_edges * 32, ns, n_cp)) + lists + pos;
+  return align_up(score_partial_bytes(n_edges * 32, ns, n_cp)) + lists + pos;
 }
 
-fastron_status fastron_edge_check(const fastron_robot* robot, const float* qa, const float* qb, int64_t n_edges,
-                                  int64_t ldq, int32_t n_interp, const float* spos, const float* alpha, int64_t ns,
-                                  int64_t lds, fastron_kernel k, uint8_t* in_collision, int32_t* hit_index,
-                                  void* workspace, size_t workspace_bytes, void* stream) {
-  NvtxRange nvtx_range_("fastron_edge_check");
+size_t fastron_edge_workspace_bytes(int64_t n_edges, int64_t ns, int32_t n_cp) {
+  if (n_edges < 0 || ns < 0 || n_cp < 1 || n_cp > FASTRON_MAX_CP) return 0;
+  return align_up(packed_bytes(ns, n_cp)) + fastron_edge_packed_workspace_bytes(n_edges, ns, n_cp);
+}
+
+}  // extern "C"
+
+namespace {
+
+// the rounds of the edge check against a packed model; ws: fastron_edge_packed_workspace_bytes
+fastron_status edge_rounds(const fastron_robot* robot, const float* qa, const float* qb, int64_t n_edges, int64_t ldq,
+                           int32_t n_interp, const float* packed, int64_t ns, fastron_kernel k, uint8_t* in_collision,
+                           int32_t* hit_index, char* ws, cudaStream_t st) {
+  const int M = robot->n_cp;
+  double* partial = reinterpret_cast<double*>(ws);
+  ws += align_up(score_partial_bytes(n_edges * 32, ns, M));
+  int32_t* counts = reinterpret_cast<int32_t*>(ws);  // [2] live counters (256 B reserved)
+  ws += 256;
+  int32_t* lists[2] = {reinterpret_cast<int32_t*>(ws), reinterpret_cast<int32_t*>(ws + align_up((size_t)n_edges * 4))};
+  ws += 2 * align_up((size_t)n_edges * 4);
+  float4* epos = reinterpret_cast<float4*>(ws);
+  const float c = kernel_scale(k);
+  const FkParams P = make_fk_params(*robot);
+  const int rounds = (n_interp + 31) / 32;
+  for (int r = 0; r < rounds; ++r) {
+    EdgeRound R;
+    R.qa = qa;
+    R.qb = qb;
+    R.ldq = ldq;
+    R.n_edges = n_edges;
+    R.n_interp = n_interp;
+    R.round = r;
+    R.active = r == 0 ? nullptr : lists[(r - 1) & 1];
+    R.active_count = r == 0 ? nullptr : counts + ((r - 1) & 1);
+    R.next_active = lists[r & 1];
+    R.next_count = counts + (r & 1);
+    R.in_collision = in_collision;
+    R.hit_index = hit_index;
+    cudaError_t e = cudaMemsetAsync(R.next_count, 0, sizeof(int32_t), st);
+    if (e != cudaSuccess) return cuda_status(e, "fastron_edge_check(memset)");
+    e = launch_edge_round(P, R, packed, ns, M, k.kind, c, partial, epos, st);
+    if (e != cudaSuccess) return cuda_status(e, "fastron_edge_check");
+  }
+  return FASTRON_OK;
+}
+
+fastron_status edge_common_checks(const fastron_robot* robot, const float* qa, const float* qb, int64_t n_edges,
+                                  int64_t ldq, int32_t n_interp, int64_t ns, fastron_kernel k, uint8_t* in_collision) {
   fastron_status s = check_robot(robot);
   if (s != FASTRON_OK) return s;
   s = check_kernel(k);
@@ -561,6 +607,20 @@ fastron_status fastron_edge_check(const fastron_robot* robot, const float* qa, c
   FASTRON_REQUIRE(n_edges <= (int64_t)1 << 26, "n_edges too large for one call (max 2^26)");
   FASTRON_REQUIRE(qa && qb && in_collision, "qa, qb and in_collision must be non-NULL");
   FASTRON_REQUIRE(ldq >= robot->dof, "ldq (%lld) < dof (%d)", (long long)ldq, robot->dof);
+  return FASTRON_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+fastron_status fastron_edge_check(const fastron_robot* robot, const float* qa, const float* qb, int64_t n_edges,
+                                  int64_t ldq, int32_t n_interp, const float* spos, const float* alpha, int64_t ns,
+                                  int64_t lds, fastron_kernel k, uint8_t* in_collision, int32_t* hit_index,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_range_("fastron_edge_check");
+  fastron_status s = edge_common_checks(robot, qa, qb, n_edges, ldq, n_interp, ns, k, in_collision);
+  if (s != FASTRON_OK || n_edges == 0) return s;
   if (ns > 0) {
     FASTRON_REQUIRE(spos && alpha, "spos and alpha must be non-NULL when ns > 0");
     FASTRON_REQUIRE(lds >= ns, "lds (%lld) < ns (%lld)", (long long)lds, (long long)ns);
@@ -578,40 +638,32 @@ fastron_status fastron_edge_check(const fastron_robot* robot, const float* qa, c
   }
   char* ws = static_cast<char*>(workspace);
   float* packed = reinterpret_cast<float*>(ws);
-  ws += align_up(packed_bytes(ns, M));
-  double* partial = reinterpret_cast<double*>(ws);
-  ws += align_up(score_partial_bytes(n_edges * 32, ns, M));
-  int32_t* counts = reinterpret_cast<int32_t*>(ws);  // [2] live counters (256 B reserved)
-  ws += 256;
-  int32_t* lists[2] = {reinterpret_cast<int32_t*>(ws), reinterpret_cast<int32_t*>(ws + align_up((size_t)n_edges * 4))};
-  ws += 2 * align_up((size_t)n_edges * 4);
-  float4* epos = reinterpret_cast<float4*>(ws);
-  const float c = kernel_scale(k);
   cudaStream_t st = S(stream);
-  cudaError_t e = launch_pack(reinterpret_cast<const float4*>(spos), lds, alpha, ns, M, c, packed, st);
+  cudaError_t e = launch_pack(reinterpret_cast<const float4*>(spos), lds, alpha, ns, M, kernel_scale(k), packed, st);
   if (e != cudaSuccess) return cuda_status(e, "fastron_edge_check(pack)");
-  const FkParams P = make_fk_params(*robot);
-  const int rounds = (n_interp + 31) / 32;
-  for (int r = 0; r < rounds; ++r) {
-    EdgeRound R;
-    R.qa = qa;
-    R.qb = qb;
-    R.ldq = ldq;
-    R.n_edges = n_edges;
-    R.n_interp = n_interp;
-    R.round = r;
-    R.active = r == 0 ? nullptr : lists[(r - 1) & 1];
-    R.active_count = r == 0 ? nullptr : counts + ((r - 1) & 1);
-    R.next_active = lists[r & 1];
-    R.next_count = counts + (r & 1);
-    R.in_collision = in_collision;
-    R.hit_index = hit_index;
-    e = cudaMemsetAsync(R.next_count, 0, sizeof(int32_t), st);
-    if (e != cudaSuccess) return cuda_status(e, "fastron_edge_check(memset)");
-    e = launch_edge_round(P, R, packed, ns, M, k.kind, c, partial, epos, st);
-    if (e != cudaSuccess) return cuda_status(e, "fastron_edge_check");
-  }
-  return FASTRON_OK;
+  return edge_rounds(robot, qa, qb, n_edges, ldq, n_interp, packed, ns, k, in_collision, hit_index,
+                     ws + align_up(packed_bytes(ns, M)), st);
+}
+
+fastron_status fastron_edge_check_packed(const fastron_robot* robot, const float* qa, const float* qb,
+                                         int64_t n_edges, int64_t ldq, int32_t n_interp, const void* packed,
+                                         int64_t ns, int32_t n_cp, fastron_kernel k, uint8_t* in_collision,
+                                         int32_t* hit_index, void* workspace, size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_range_("fastron_edge_check_packed");
+  fastron_status s = edge_common_checks(robot, qa, qb, n_edges, ldq, n_interp, ns, k, in_collision);
+  if (s != FASTRON_OK || n_edges == 0) return s;
+  FASTRON_REQUIRE(n_cp == robot->n_cp, "n_cp (%d) differs from robot->n_cp (%d)", n_cp, robot->n_cp);
+  FASTRON_REQUIRE(ns == 0 || packed, "packed is NULL");
+  FASTRON_REQUIRE(ns == 0 || ((uintptr_t)packed & 255) == 0, "packed must be 256-byte aligned (fastron_model_pack)");
+  const size_t need = fastron_edge_packed_workspace_bytes(n_edges, ns, n_cp);
+  if (workspace_bytes < need || !workspace)
+    return fail(FASTRON_ERR_WORKSPACE, "fastron_edge_check_packed needs %zu workspace bytes, got %zu", need,
+                workspace_bytes);
+  FASTRON_REQUIRE(((uintptr_t)workspace & 255) == 0, "workspace must be 256-byte aligned");
+  FASTRON_VALIDATE(vcheck_f32(qa, n_edges, robot->dof, ldq, stream, "qa"));
+  FASTRON_VALIDATE(vcheck_f32(qb, n_edges, robot->dof, ldq, stream, "qb"));
+  return edge_rounds(robot, qa, qb, n_edges, ldq, n_interp, static_cast<const float*>(packed), ns, k, in_collision,
+                     hit_index, static_cast<char*>(workspace), S(stream));
 }
 
 size_t fastron_score_joint_workspace_bytes(int64_t nq, int64_t ns, int32_t dof) {
@@ -783,11 +835,19 @@ fastron_status fastron_query(const fastron_robot* robot, const float* q, int64_t
   // last wave leaves idle, and chunk c+2 reuses chunk c's buffers
   cudaStream_t h2d = query_copy_stream(0), d2h = query_copy_stream(1);
   cudaStream_t cs[2] = {st, query_copy_stream(2)};
-  cudaEvent_t ev_in[2], ev_used[2], ev_out[2];
+  // the pipeline's 6 events are created once per host thread and device (a call ends with
+  // a synchronisation, so the next call on this thread may reuse them)
+  static thread_local cudaEvent_t t_events[64][6] = {};
+  int evdev = 0;
+  cudaGetDevice(&evdev);
+  if (evdev < 0 || evdev >= 64) evdev = 0;
+  cudaEvent_t* evs = t_events[evdev];
+  if (!evs[0])
+    for (int i = 0; i < 6; ++i) cudaEventCreateWithFlags(&evs[i], cudaEventDisableTiming);
+  cudaEvent_t* ev_in = evs;
+  cudaEvent_t* ev_used = evs + 2;
+  cudaEvent_t* ev_out = evs + 4;
   for (int b = 0; b < 2; ++b) {
-    cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev_used[b], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev_out[b], cudaEventDisableTiming);
     cudaEventRecord(ev_used[b], st);  // ordered after the model pack and earlier work on `stream`
     cudaEventRecord(ev_out[b], st);
   }
@@ -830,11 +890,6 @@ fastron_status fastron_query(const fastron_robot* robot, const float* q, int64_t
   cudaError_t e2 = cudaStreamSynchronize(h2d);
   cudaError_t e3 = cudaStreamSynchronize(d2h);
   cudaError_t e4 = cudaStreamSynchronize(st);
-  for (int b = 0; b < 2; ++b) {
-    cudaEventDestroy(ev_in[b]);
-    cudaEventDestroy(ev_used[b]);
-    cudaEventDestroy(ev_out[b]);
-  }
   if (e == cudaSuccess) e = e2;
   if (e == cudaSuccess) e = e3;
   if (e == cudaSuccess) e = e4;

@@ -478,6 +478,7 @@ __global__ void __launch_bounds__(256) finalize_grouped_kernel(const __grid_cons
 // Terms, lane sums and fp64 accumulation are those of K2 (same tolerance).
 constexpr int kSmallQ = 32;
 constexpr int kSmallNT = 256;
+constexpr int kSmallChunk = 32;  // CTA partials fetched per round by the last CTA
 
 // FUSED_FK: the queries arrive as configurations and thread q runs the D-H chain of
 // query q (fk_chain, the FK kernel's arithmetic and rounding: the same positions), so a
@@ -490,11 +491,19 @@ __global__ void __launch_bounds__(kSmallNT) score_small_kernel(const __grid_cons
   constexpr int64_t TF = tile_floats(MP);
   __shared__ f2 sq[kSmallQ][NP][3];
   __shared__ double s_red[kSmallNT / 32][kSmallQ];
+  __shared__ double s_fin[kSmallChunk][kSmallQ];
   __shared__ float s_pos[FUSED_FK ? kSmallQ : 1][FUSED_FK ? MP : 1][3];
   __shared__ int s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nq = (int)A.nq;
   if (FUSED_FK) {
+    // the thread's first support record travels to L1 while the D-H chains run
+    const int64_t sup0 = (int64_t)blockIdx.x * kSmallNT + tid;
+    if (sup0 < ns) {
+      const float* r0 = A.packed + (sup0 / kTileSupports) * TF + (sup0 % kTileSupports) * NP * 8;
+#pragma unroll
+      for (int p = 0; p < NP; ++p) asm volatile("prefetch.global.L1 [%0];" ::"l"(r0 + p * 8));
+    }
     if (tid < nq) {
       const float* qk = A.qcfg + (int64_t)tid * A.ldqc;
       fk_chain(
@@ -586,11 +595,20 @@ __global__ void __launch_bounds__(kSmallNT) score_small_kernel(const __grid_cons
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  if (tid < nq) {
-    double v = 0.0;
-    for (unsigned c = 0; c < gridDim.x; ++c) v += __ldcg(A.partial + (int64_t)c * kSmallQ + tid);
-    write_score(A, tid, v);
+  // the last CTA adds the CTA partials in CTA order; all its threads fetch a chunk of them at
+  // once into shared memory first (one L2 round trip per 64 CTAs instead of one per CTA on
+  // a serial chain: 1 query x 20k supports, 79 CTAs: 18.3 us before), same order, same bits
+  double v = 0.0;
+  for (unsigned c0 = 0; c0 < gridDim.x; c0 += kSmallChunk) {
+    const unsigned cn = min((unsigned)kSmallChunk, gridDim.x - c0);
+    for (unsigned i = tid; i < cn * kSmallQ; i += kSmallNT)
+      s_fin[i / kSmallQ][i % kSmallQ] = __ldcg(A.partial + (int64_t)(c0 + i / kSmallQ) * kSmallQ + i % kSmallQ);
+    __syncthreads();
+    if (tid < nq)
+      for (unsigned c = 0; c < cn; ++c) v += s_fin[c][tid];
+    __syncthreads();
   }
+  if (tid < nq) write_score(A, tid, v);
   if (tid == 0) *ticket = 0u;  // reset for the next call on this workspace
 }
 

@@ -132,3 +132,20 @@ def test_odd_m_robot_edges():
     rng = np.random.default_rng(5)
     robot = W.make_robot("m5", wl.robot.dh, rng.integers(1, 8, size=5), rng.uniform(-0.1, 0.1, size=(5, 3)))
     _check(robot, wl.qa, wl.qb, wl.n_interp, wl.supports, wl.alpha, 0, wl.gamma)
+
+
+@pytest.mark.parametrize("kind", [W.GAUSSIAN, W.RQ])
+def test_edge_check_packed_equals_edge_check(kind):
+    """The packed-model edge check (a model packed once, e.g. broadcast to every GPU) gives
+    exactly fastron_edge_check's flags and hit indices."""
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    wl = W.edge_workload(n_edges=2000, kind=kind)
+    spos = fb.fastron_fk(wl.robot, dev(wl.supports))
+    qa, qb = dev(wl.qa), dev(wl.qb)
+    h1, i1 = fb.fastron_edge_check(wl.robot, qa, qb, wl.n_interp, spos, dev(wl.alpha), kind, wl.gamma)
+    model = fb.fastron_model_pack(spos, dev(wl.alpha), kind, wl.gamma)
+    h2, i2 = fb.fastron_edge_check_packed(wl.robot, qa, qb, wl.n_interp, model)
+    torch.cuda.synchronize()
+    assert torch.equal(h1, h2) and torch.equal(i1, i2) and 0 < int(h1.sum()) < len(h1)

@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "../paper_1910_06451_b200/csrc/fastron_device.cuh"
+
 #define CK(x) do{cudaError_t e=(x); if(e!=cudaSuccess){printf("CUDA %s @%d\n",cudaGetErrorString(e),__LINE__); return 1;}}while(0)
 
 __device__ __forceinline__ uint64_t gtimer(){ uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
@@ -24,7 +26,10 @@ __global__ void __launch_bounds__(256) bench(float seed, int iters, float* out, 
 #pragma unroll
     for (int c = 0; c < CHAINS; ++c) {
       if (OP == 0) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(v[c]));
-      if (OP == 1) asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(v[c]));
+      if (OP == 1) {  // rcp(rcp(x)) folds away (round 1 measured an impossible 2,120/clk): perturb
+        asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(v[c]));
+        asm volatile("mul.rn.f32 %0, %0, %1;" : "+f"(v[c]) : "f"(seed));
+      }
       if (OP == 2) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(v[c]) : "f"(seed), "f"(v[(c+1)%CHAINS]));
       if (OP == 3) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(p[c]) : "l"(p[(c+3)%CHAINS]), "l"(p[(c+1)%CHAINS]));
       if (OP == 4) asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(p[c]) : "l"(p[(c+1)%CHAINS]));
@@ -98,6 +103,39 @@ __global__ void __launch_bounds__(256) bench_term_scalar(float seed, int iters, 
   if (threadIdx.x == 0) rec[blockIdx.x] = Rec{c0, c1, t0, t1};
 }
 
+// The product's term function (fastron_device.cuh accum_term) on 4 control-point pairs x
+// QT = 3 queries per support, as the scoring kernel issues it; KIND 0 = Gaussian (7 packed
+// FP32 ops + 2 MUFU per pair), 1 = RQ with the Newton step (11 + 2). The support operand
+// changes every iteration (no hoisting); the accumulators are written out (no dead code).
+template <int KIND>
+__global__ void __launch_bounds__(128) bench_accum(float seed, int iters, float* out, Rec* rec) {
+  fastron::f2 ux[3][4], uy[3][4], uz[3][4];
+  for (int j = 0; j < 3; ++j)
+    for (int p = 0; p < 4; ++p) {
+      const float b = seed * (threadIdx.x + 7 * j + p) * 1e-3f;
+      ux[j][p] = fastron::pk(b, b + 0.1f); uy[j][p] = fastron::pk(0.5f * b, b); uz[j][p] = fastron::pk(0.25f * b, 0.3f);
+    }
+  fastron::f2 vx = fastron::pk(0.1f, 0.2f), vy = fastron::pk(0.3f, 0.1f), vz = fastron::pk(0.2f, 0.4f);
+  const fastron::f2 dv = fastron::pk(1e-6f, -1e-6f);
+  double f[3] = {0.0, 0.0, 0.0};
+  __syncthreads();
+  unsigned long long c0 = clock64(); uint64_t t0 = gtimer();
+  for (int it = 0; it < iters; ++it) {
+    fastron::f2 acc[3];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        fastron::accum_term<KIND>(acc[j], fastron::sub2(ux[j][p], vx), fastron::sub2(uy[j][p], vy), fastron::sub2(uz[j][p], vz), p == 0);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) f[j] += (double)fastron::lo(acc[j]) + (double)fastron::hi(acc[j]);
+    vx = fastron::add2(vx, dv); vy = fastron::add2(vy, dv); vz = fastron::add2(vz, dv);
+  }
+  unsigned long long c1 = clock64(); uint64_t t1 = gtimer();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = (float)(f[0] + f[1] + f[2]);
+  if (threadIdx.x == 0) rec[blockIdx.x] = Rec{c0, c1, t0, t1};
+}
+
 int main() {
   int dev = 0; cudaDeviceProp prop; CK(cudaGetDeviceProperties(&prop, dev));
   int sms = prop.multiProcessorCount;
@@ -105,8 +143,9 @@ int main() {
   const int blocks = sms * 4, threads = 256, iters = 4096;
   float* out; Rec* rec; CK(cudaMalloc(&out, blocks * threads * 4)); CK(cudaMalloc(&rec, blocks * sizeof(Rec)));
   Rec* h = new Rec[blocks];
-  const char* names[] = {"mufu_ex2", "mufu_rcp", "ffma", "ffma2", "fadd2", "dadd", "dfma", "fadd", "term_pair", "term_scalar"};
-  for (int op = 0; op < 10; ++op) {
+  const char* names[] = {"mufu_ex2", "mufu_rcp", "ffma", "ffma2", "fadd2", "dadd", "dfma", "fadd", "term_pair",
+                         "term_scalar", "accum_gaussian_terms", "accum_rq_newton_terms"};
+  for (int op = 0; op < 12; ++op) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
       cudaEventRecord(e0);
@@ -121,6 +160,8 @@ int main() {
         case 7: bench<7><<<blocks, threads>>>(1.0001f, iters, out, rec); break;
         case 8: bench_term<<<blocks, threads>>>(1.0001f, iters, out, rec); break;
         case 9: bench_term_scalar<<<blocks, threads>>>(1.0001f, iters, out, rec); break;
+        case 10: bench_accum<0><<<blocks, 128>>>(1.0001f, iters / 4, out, rec); break;
+        case 11: bench_accum<1><<<blocks, 128>>>(1.0001f, iters / 4, out, rec); break;
       }
       CK(cudaGetLastError());
       cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
@@ -131,8 +172,9 @@ int main() {
       for (int b = 0; b < blocks; ++b) { clk += (double)(h[b].clk1 - h[b].clk0); ns += (double)(h[b].t1 - h[b].t0); }
       clk /= blocks; ns /= blocks;
       double mhz = clk / ns * 1e3;
-      int it = (op == 5 || op == 6) ? iters / 4 : iters;
+      int it = (op == 5 || op == 6 || op >= 10) ? iters / 4 : iters;
       double ops_per_block = (double)threads * it * (op >= 8 ? 8 : CHAINS);  // op 8: 4 pairs x 2 MUFU terms
+      if (op >= 10) ops_per_block = 128.0 * it * 24;  // 3 queries x 8 terms (one MUFU each) per iteration
       // blocks resident 4/SM (256 thr, low regs) -> per-SM ops per clock = 4 * ops_per_block / clk
       // per-SM rate from the event time and the measured clock (robust to residency)
       double per_sm_clk = (double)blocks * ops_per_block / (ms * 1e-3) / sms / (mhz * 1e6);
