@@ -101,27 +101,24 @@ def test_edge_equals_or_of_scores():
     assert np.array_equal(hit.astype(bool), any_pos)
 
 
-def test_cfg4_full_size_sampled():
+@pytest.mark.parametrize("kind", [W.GAUSSIAN, W.RQ])
+def test_cfg4_full_size_all_edges(kind):
     """cfg4 at its full size (10,000 edges x 64 points against 3,000 supports, the bench
-    launch): the oracle re-checks 300 seeded edges plus 100 of the edges the GPU reports
-    in collision (hit labels, and the reported point really has f > 0)."""
+    launch), every edge against the oracle: labels bit-exact wherever
+    the edge's max score is outside +-1e-4, and every reported hit point really has
+    f_ref > -1e-4; misses report -1."""
     require_gpu()
-    wl = W.edge_workload()
+    wl = W.edge_workload(kind=kind)
     assert len(wl.qa) == 10_000 and wl.n_interp == 64 and len(wl.supports) == 3_000
-    hit, idx = _gpu_edges(wl.robot, wl.qa, wl.qb, wl.n_interp, wl.supports, wl.alpha, 0, wl.gamma)
-    rng = np.random.default_rng(4)
-    hits = np.flatnonzero(hit)
-    sample = np.unique(np.concatenate([rng.choice(len(hit), 300, replace=False),
-                                       rng.choice(hits, min(100, hits.size), replace=False)]))
-    ref_hit, fmax, fall = oracle.edge(wl.robot, wl.qa[sample], wl.qb[sample], wl.n_interp, 0, wl.gamma,
+    hit, idx = _gpu_edges(wl.robot, wl.qa, wl.qb, wl.n_interp, wl.supports, wl.alpha, kind, wl.gamma)
+    ref_hit, fmax, fall = oracle.edge(wl.robot, wl.qa, wl.qb, wl.n_interp, kind, wl.gamma,
                                       oracle.fk(wl.robot, wl.supports), wl.alpha, with_all=True)
     sure = np.abs(fmax) > 1e-4
-    assert np.array_equal(hit[sample][sure], ref_hit[sure])
-    for e, s_e in enumerate(sample):
-        if hit[s_e]:
-            assert fall[e, idx[s_e]] > -1e-4
-        else:
-            assert idx[s_e] == -1
+    assert np.array_equal(hit[sure], ref_hit[sure])
+    h = np.flatnonzero(hit)
+    assert np.all(fall[h, idx[h]] > -1e-4)
+    assert np.all(idx[hit == 0] == -1)
+    print(f"cfg4 kind={kind}: {int(hit.sum())} of 10,000 in collision, {int((~sure).sum())} ambiguous")
 
 
 def test_odd_m_robot_edges():
