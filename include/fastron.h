@@ -334,6 +334,26 @@ fastron_status fastron_query_packed(const fastron_robot* robot, const float* q, 
                                     const void* packed, int64_t ns, int32_t n_cp, fastron_kernel k, float* score,
                                     int8_t* label, void* workspace, size_t workspace_bytes, void* stream);
 
+/*
+ * The fp64 path for ill-conditioned models (R25). A model trained by
+ * Algorithm 1 has weights of both signs up to ~200, so its score
+ * cancels and the fp32 path's rounding (~1e-5..1e-4) can exceed the 1e-5
+ * floor near the decision boundary. These calls keep the positions, the weights, every
+ * term of Eq. 3/4 and every sum in fp64.
+ * fastron_fk64 — fastron_fk with unrounded fp64 positions: pos device double4
+ *   [n_cp][ldpos] = (x, y, z, 0), 32-byte aligned, ldpos >= n.
+ * fastron_score_precise — f(q) = sum_i alpha_i (1/M) sum_m t_m in fp64 (Gaussian exp, RQ
+ *   by division), support order. qpos: double4 [n_cp][ldq] (fastron_fk64), spos: double4
+ *   [n_cp][lds], alpha: device double [ns] (e.g. fastron_train's alpha), score: device
+ *   double [nq] (nullable), label: int8 [nq] (nullable; +1 iff f > 0). n_cp <= 16 (else
+ *   UNSUPPORTED). No workspace. Roughly 10x the fp32 path's time per term.
+ */
+fastron_status fastron_fk64(const fastron_robot* robot, const float* q, int64_t n, int64_t ldq, double* pos,
+                            int64_t ldpos, void* stream);
+fastron_status fastron_score_precise(const double* qpos, int64_t nq, int64_t ldq, const double* spos,
+                                     const double* alpha, int64_t ns, int64_t lds, int32_t n_cp, fastron_kernel k,
+                                     double* score, int8_t* label, void* stream);
+
 /* Thread-local message for the last non-OK status returned on this thread. */
 const char* fastron_last_error(void);
 

@@ -137,11 +137,14 @@ def kernel_value(kind, gamma, u, v) -> float:
                                            _p(v, ctypes.c_double)))
 
 
-def score(kind, gamma, qpos, spos, alpha):
-    """f (nq,) float64 and labels (nq,) int8 for positions qpos (nq, M, 3), spos (ns, M, 3)."""
+def score(kind, gamma, qpos, spos, alpha, exact_alpha=False):
+    """f (nq,) float64 and labels (nq,) int8 for positions qpos (nq, M, 3), spos (ns, M, 3).
+    alpha is taken as fp32 values (the inputs of the fp32 path) unless exact_alpha, when
+    fp64 weights are used unrounded (the fp64 path scores Algorithm 1's fp64 alpha)."""
     qpos = np.ascontiguousarray(np.asarray(qpos, dtype=np.float64))
     spos = np.ascontiguousarray(np.asarray(spos, dtype=np.float64))
-    alpha = np.ascontiguousarray(np.asarray(alpha, dtype=np.float32).astype(np.float64))
+    alpha = np.ascontiguousarray(np.asarray(alpha, dtype=np.float64) if exact_alpha else
+                                 np.asarray(alpha, dtype=np.float32).astype(np.float64))
     nq, M = qpos.shape[0], qpos.shape[1]
     ns = spos.shape[0]
     f = np.zeros(nq)

@@ -35,7 +35,7 @@ EXPORTED = [
     "fastron_kernel_matvec", "fastron_score_packed_f64", "fastron_set_validation", "fastron_validation",
     "fastron_kernel_matvec_lazy_workspace_bytes", "fastron_kernel_matvec_lazy",
     "fastron_query_packed_workspace_bytes", "fastron_query_packed",
-    "fastron_edge_packed_workspace_bytes", "fastron_edge_check_packed",
+    "fastron_edge_packed_workspace_bytes", "fastron_edge_check_packed", "fastron_fk64", "fastron_score_precise",
 ]
 
 
@@ -118,6 +118,8 @@ def load_library(path: str = LIB_PATH):
     L.fastron_edge_workspace_bytes.argtypes = [i64, i64, i32]
     L.fastron_edge_workspace_bytes.restype = sz
     L.fastron_edge_check.argtypes = [rp, vp, vp, i64, i64, i32, vp, vp, i64, i64, fastron_kernel, vp, vp, vp, sz, vp]
+    L.fastron_fk64.argtypes = [rp, vp, i64, i64, vp, i64, vp]
+    L.fastron_score_precise.argtypes = [vp, i64, i64, vp, vp, i64, i64, i32, fastron_kernel, vp, vp, vp]
     L.fastron_edge_packed_workspace_bytes.argtypes = [i64, i64, i32]
     L.fastron_edge_packed_workspace_bytes.restype = sz
     L.fastron_edge_check_packed.argtypes = [rp, vp, vp, i64, i64, i32, vp, i64, i32, fastron_kernel, vp, vp, vp, sz,
@@ -131,7 +133,8 @@ def load_library(path: str = LIB_PATH):
     for f in ("fastron_fk", "fastron_score", "fastron_gram", "fastron_train", "fastron_edge_check", "fastron_query",
               "fastron_model_pack", "fastron_score_packed", "fastron_score_joint", "fastron_gram_joint", "fastron_train_lazy", "fastron_active_samples",
               "fastron_label_capsules", "fastron_kernel_matvec", "fastron_score_packed_f64",
-              "fastron_kernel_matvec_lazy", "fastron_query_packed", "fastron_edge_check_packed"):
+              "fastron_kernel_matvec_lazy", "fastron_query_packed", "fastron_edge_check_packed", "fastron_fk64",
+              "fastron_score_precise"):
         getattr(L, f).restype = st
     L.fastron_last_error.argtypes = []
     L.fastron_last_error.restype = ctypes.c_char_p
@@ -684,6 +687,49 @@ def fastron_query_packed(robot, q, model: PackedModel, score=None, label=None, w
     _check(L.fastron_query_packed(ctypes.byref(r), _ptr(q), nq, q.stride(0), _ptr(model.buf), model.ns, r.n_cp,
                                   _kernel(model.kind, model.gamma), _ptr(score), _ptr(label), _ptr(workspace),
                                   workspace.numel(), ts.cuda_stream))
+    return score, label
+
+
+def fastron_fk64(robot, q, pos=None, stream=None):
+    """q (n, >=D) float32 cuda -> pos (M, n, 4) float64 cuda: unrounded fp64 positions."""
+    torch = _torch()
+    L = load_library()
+    _require_cuda(q, pos)
+    _expect(q, torch.float32, "q", dim=2)
+    r = robot if isinstance(robot, fastron_robot) else make_robot_struct(robot)
+    n = q.shape[0]
+    ts = _tstream(stream)
+    if pos is None:
+        pos = _new((r.n_cp, n, 4), torch.float64, q.device, ts)
+    _expect(pos, torch.float64, "pos", dim=3)
+    if pos.shape[0] != r.n_cp or pos.shape[2] != 4 or (n > 1 and pos.stride(1) != 4) or pos.data_ptr() % 32:
+        raise ValueError("pos must be (M, n, 4) float64 with 32-byte aligned double4 records")
+    _check(L.fastron_fk64(ctypes.byref(r), _ptr(q), n, q.stride(0), _ptr(pos), pos.stride(0) // 4, ts.cuda_stream))
+    return pos
+
+
+def fastron_score_precise(qpos64, spos64, alpha64, kind: int, gamma: float, score=None, label=None, stream=None):
+    """fp64 scores (nq,) float64 and labels of fp64 positions against fp64 supports/weights."""
+    torch = _torch()
+    L = load_library()
+    _require_cuda(qpos64, spos64, alpha64, score, label)
+    for t, nm in ((qpos64, "qpos64"), (spos64, "spos64")):
+        _expect(t, torch.float64, nm, dim=3)
+        if t.shape[2] != 4 or (t.shape[1] > 1 and t.stride(1) != 4) or (t.numel() and t.data_ptr() % 32):
+            raise ValueError(f"{nm} must be (M, n, 4) float64 with 32-byte aligned double4 records")
+    _expect(alpha64, torch.float64, "alpha64", dim=1)
+    M, nq = qpos64.shape[0], qpos64.shape[1]
+    ns = spos64.shape[1]
+    ts = _tstream(stream)
+    if score is None:
+        score = _new(nq, torch.float64, qpos64.device, ts)
+    if label is None:
+        label = _new(nq, torch.int8, qpos64.device, ts)
+    _expect(score, torch.float64, "score", dim=1)
+    _expect(label, torch.int8, "label", dim=1)
+    _check(L.fastron_score_precise(_ptr(qpos64), nq, qpos64.stride(0) // 4, _ptr(spos64) if ns else None,
+                                   _ptr(alpha64) if ns else None, ns, spos64.stride(0) // 4 if ns else 0, M,
+                                   _kernel(kind, gamma), _ptr(score), _ptr(label), ts.cuda_stream))
     return score, label
 
 

@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libfastron_b200.so")
 BUILD = os.path.join(ROOT, "build", "obj")
-SOURCES = ["abi.cu", "fk.cu", "score.cu", "gram.cu", "train.cu", "update.cu", "validate.cu"]
+SOURCES = ["abi.cu", "fk.cu", "score.cu", "gram.cu", "train.cu", "update.cu", "validate.cu", "precise.cu"]
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-diag-suppress=128",

@@ -344,6 +344,51 @@ fastron_status fastron_score_packed(const float* qpos, int64_t nq, int64_t ldq, 
                      "fastron_score_packed");
 }
 
+fastron_status fastron_fk64(const fastron_robot* robot, const float* q, int64_t n, int64_t ldq, double* pos,
+                            int64_t ldpos, void* stream) {
+  NvtxRange nvtx_range_("fastron_fk64");
+  fastron_status s = check_robot(robot);
+  if (s != FASTRON_OK) return s;
+  FASTRON_REQUIRE(n >= 0, "n must be >= 0");
+  if (n == 0) return FASTRON_OK;
+  FASTRON_REQUIRE(q && pos, "q and pos must be non-NULL");
+  FASTRON_REQUIRE(ldq >= robot->dof, "ldq (%lld) < dof (%d)", (long long)ldq, robot->dof);
+  FASTRON_REQUIRE(ldpos >= n, "ldpos (%lld) < n (%lld)", (long long)ldpos, (long long)n);
+  FASTRON_REQUIRE(((uintptr_t)pos & 31) == 0, "pos must be 32-byte aligned (double4 records)");
+  FASTRON_VALIDATE(vcheck_f32(q, n, robot->dof, ldq, stream, "q"));
+  return cuda_status(launch_fk64(make_fk_params(*robot), q, n, ldq, reinterpret_cast<double4*>(pos), ldpos, S(stream)),
+                     "fastron_fk64");
+}
+
+fastron_status fastron_score_precise(const double* qpos, int64_t nq, int64_t ldq, const double* spos,
+                                     const double* alpha, int64_t ns, int64_t lds, int32_t n_cp, fastron_kernel k,
+                                     double* score, int8_t* label, void* stream) {
+  NvtxRange nvtx_range_("fastron_score_precise");
+  fastron_status s = check_kernel(k);
+  if (s != FASTRON_OK) return s;
+  FASTRON_REQUIRE(nq >= 0 && ns >= 0, "nq and ns must be >= 0");
+  FASTRON_REQUIRE(n_cp >= 1 && n_cp <= FASTRON_MAX_CP, "n_cp must be in [1,32], got %d", n_cp);
+  if (n_cp > 16) return fail(FASTRON_ERR_UNSUPPORTED, "fastron_score_precise supports n_cp <= 16, got %d", n_cp);
+  if (nq == 0) return FASTRON_OK;
+  FASTRON_REQUIRE(qpos != nullptr && ldq >= nq, "qpos must be non-NULL and ldq >= nq");
+  FASTRON_REQUIRE(score || label, "score and label are both NULL");
+  FASTRON_REQUIRE(((uintptr_t)qpos & 31) == 0, "qpos must be 32-byte aligned (double4 records)");
+  if (ns > 0) {
+    FASTRON_REQUIRE(spos && alpha, "spos and alpha must be non-NULL when ns > 0");
+    FASTRON_REQUIRE(lds >= ns, "lds (%lld) < ns (%lld)", (long long)lds, (long long)ns);
+    FASTRON_REQUIRE(((uintptr_t)spos & 31) == 0, "spos must be 32-byte aligned (double4 records)");
+  }
+  FASTRON_VALIDATE(vcheck_f64(qpos, 4 * ldq * n_cp, stream, "qpos"));
+  if (ns > 0) {
+    FASTRON_VALIDATE(vcheck_f64(spos, 4 * lds * n_cp, stream, "spos"));
+    FASTRON_VALIDATE(vcheck_f64(alpha, ns, stream, "alpha"));
+  }
+  return cuda_status(launch_score64(reinterpret_cast<const double4*>(qpos), nq, ldq,
+                                    reinterpret_cast<const double4*>(spos), alpha, ns, lds, n_cp, k.kind,
+                                    (double)k.gamma, score, label, S(stream)),
+                     "fastron_score_precise");
+}
+
 fastron_status fastron_score_packed_f64(const float* qpos, int64_t nq, int64_t ldq, const void* packed, int64_t ns,
                                         int32_t n_cp, fastron_kernel k, double* score64, void* workspace,
                                         size_t workspace_bytes, void* stream) {

@@ -97,6 +97,13 @@ cudaError_t launch_matvec(const float* K, int64_t n, int64_t ldk, const double* 
 cudaError_t launch_matvec_lazy(const float* packed, int64_t n, int M, int kind, const double* alpha, double* F,
                                cudaStream_t st);
 
+// fp64 path for ill-conditioned (trained) models (precise.cu)
+cudaError_t launch_fk64(const FkParams& P, const float* q, int64_t n, int64_t ldq, double4* pos, int64_t ldpos,
+                        cudaStream_t st);
+cudaError_t launch_score64(const double4* qpos, int64_t nq, int64_t ldq, const double4* spos, const double* alpha,
+                           int64_t ns, int64_t lds, int M, int kind, double gamma, double* score, int8_t* label,
+                           cudaStream_t st);
+
 // Optional content checks (validate.cu): counts are read back synchronously.
 cudaError_t count_nonfinite(const float* a, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st,
                             unsigned long long* out);

@@ -11,7 +11,8 @@ from typing import Optional
 
 import numpy as np
 
-from . import (fastron_active_samples, fastron_fk, fastron_gram, fastron_kernel_matvec, fastron_kernel_matvec_lazy,
+from . import (fastron_active_samples, fastron_fk, fastron_fk64, fastron_gram, fastron_kernel_matvec,
+               fastron_kernel_matvec_lazy, fastron_score_precise,
                fastron_label_capsules, fastron_model_pack, fastron_query_packed, fastron_score_packed, fastron_train,
                fastron_train_lazy,
                make_robot_struct, train_result)
@@ -31,11 +32,15 @@ class CapsuleScene:
 
 class FastronModel:
     def __init__(self, robot, kind: int = 0, gamma: float = 5.0, beta: float = 1.0, iter_max: int = 20000,
-                 s_max: Optional[int] = None, lazy: bool = False, cache_cols: int = 4096):
+                 s_max: Optional[int] = None, lazy: bool = False, cache_cols: int = 4096, precise: bool = False):
         self.robot = robot
         self.robot_c = make_robot_struct(robot)
         self.kind, self.gamma, self.beta = int(kind), float(gamma), float(beta)
         self.iter_max, self.s_max, self.lazy, self.cache_cols = int(iter_max), s_max, bool(lazy), int(cache_cols)
+        # precise: queries are scored on the fp64 path (unrounded positions, fp64 weights and
+        # terms) — for trained models whose cancelling sums the fp32 path cannot resolve to
+        # 1e-5 near the decision boundary (R25)
+        self.precise = bool(precise)
         self.supports = None  # (|S|, D) device float32 configurations
         self.alpha = None  # (|S|,) device float64
         self.last = None  # result dict of the last training run
@@ -68,6 +73,7 @@ class FastronModel:
     def _pack(self):
         spos = fastron_fk(self.robot_c, self.supports)
         self.model = fastron_model_pack(spos, self.alpha.float(), self.kind, self.gamma)
+        self.spos64 = fastron_fk64(self.robot_c, self.supports) if self.precise else None
 
     def fit(self, X, y):
         """X: (N, D) float32 device configurations, y: (N,) int8 device labels (+1 = C_obs)."""
@@ -113,7 +119,10 @@ class FastronModel:
     # ---- proxy collision check ----
     def query(self, q):
         """Configurations q (n, D) device float32 -> (score, label): fastron_query_packed
-        (one launch for small and mid-size batches)."""
+        (one launch for small batches); precise models: fastron_fk64 + fastron_score_precise
+        (fp64 scores)."""
+        if self.precise:
+            return fastron_score_precise(fastron_fk64(self.robot_c, q), self.spos64, self.alpha, self.kind, self.gamma)
         return fastron_query_packed(self.robot_c, q, self.model)
 
     def query_graph(self, nq: int):
@@ -131,9 +140,18 @@ class FastronModel:
         ws = torch.empty(max(256, load_library().fastron_query_packed_workspace_bytes(
             nq, self.model.ns, self.model.n_cp, self.robot_c.dof)), dtype=torch.uint8, device=dev)
         model = self.model
+        if self.precise:  # fp64 path: static fp64 positions and scores
+            score = torch.empty(nq, dtype=torch.float64, device=dev)
+            qpos64 = torch.empty((self.robot_c.n_cp, nq, 4), dtype=torch.float64, device=dev)
+            spos64 = self.spos64
 
-        def body():
-            fastron_query_packed(self.robot_c, q_static, model, score, label, workspace=ws)
+            def body():
+                fastron_fk64(self.robot_c, q_static, pos=qpos64)
+                fastron_score_precise(qpos64, spos64, self.alpha, self.kind, self.gamma, score=score, label=label)
+            ws = (ws, qpos64, spos64)
+        else:
+            def body():
+                fastron_query_packed(self.robot_c, q_static, model, score, label, workspace=ws)
 
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())

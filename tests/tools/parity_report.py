@@ -98,6 +98,15 @@ def trained_case(kind):
     st.update(n_support=int(res["n_support"]), max_abs_alpha=float(np.abs(a32).max()),
               ill_conditioned_kappa_gt_1e4=int(np.sum(kappa > 1e4)),
               max_err_over_condition=float(np.max(np.abs(s - f) / cond)))
+    ok = kappa <= 1e4
+    st["non_cancelling_queries"] = score_stats(s[ok], f[ok], l[ok])
+    # the same model on the fp64 path (fastron_fk64 + fastron_score_precise, fp64 alpha)
+    import paper_1910_06451_b200 as fbm
+    s64, l64 = fbm.fastron_score_precise(fbm.fastron_fk64(tw.robot, torch.from_numpy(q).cuda()),
+                                         fbm.fastron_fk64(tw.robot, m.supports), m.alpha, kind, tw.gamma)
+    torch.cuda.synchronize()
+    f64, _ = oracle.score(kind, tw.gamma, qp, sp, m.alpha.cpu().numpy(), exact_alpha=True)
+    st["fp64_path_every_query"] = score_stats(s64.cpu().numpy(), f64, l64.cpu().numpy())
     return st
 
 
