@@ -106,7 +106,8 @@ fastron_status fastron_fk(const fastron_robot* robot, const float* q, int64_t n,
 /*
  * fastron_score — Fastron model evaluation f(x) = sum_i K_FK(S_i, x) alpha_i and its
  * sign, K_FK of Eq. 4 with the term of k.kind.
- *   qpos: device float4 [n_cp][ldq] query control points (from fastron_fk), ldq >= nq.
+ *   qpos: device float4 [n_cp][ldq] query control points (from fastron_fk), ldq >= nq,
+ *   16-byte aligned (as spos).
  *   spos: device float4 [n_cp][lds] support control points, lds >= ns. alpha: device float [ns].
  *   score: device float [nq] (nullable): f rounded to fp32 (accumulated in fp64).
  *   label: device int8 [nq] (nullable): +1 iff f > 0 else -1 (R8).
@@ -133,8 +134,10 @@ fastron_status fastron_score(const float* qpos, int64_t nq, int64_t ldq, const f
  *   fastron_model_bytes(ns, n_cp) bytes, 256-byte aligned, holding the supports
  *   pre-scaled for kernel k (its contents are only meaningful to fastron_score_packed
  *   with the same ns, n_cp and k).
- *   fastron_score_packed: qpos/score/label as fastron_score; workspace >=
- *   fastron_score_packed_workspace_bytes(nq, ns, n_cp) (may be 0 bytes).
+ *   fastron_score_packed: qpos/score/label as fastron_score (qpos 16-byte aligned);
+ *   packed as written by fastron_model_pack (256-byte aligned, checked); workspace >=
+ *   fastron_score_packed_workspace_bytes(nq, ns, n_cp) (may be 0 bytes), 256-byte aligned
+ *   when non-empty (checked: misaligned buffers return INVALID_ARG, never a fault).
  */
 size_t fastron_model_bytes(int64_t ns, int32_t n_cp);
 /* fastron_score_packed_f64: the same scores in fp64 (before the fp32 rounding). score64:

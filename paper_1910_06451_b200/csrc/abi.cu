@@ -264,10 +264,12 @@ fastron_status fastron_score(const float* qpos, int64_t nq, int64_t ldq, const f
   if (nq == 0) return FASTRON_OK;
   FASTRON_REQUIRE(qpos != nullptr, "qpos is NULL");
   FASTRON_REQUIRE(ldq >= nq, "ldq (%lld) < nq (%lld)", (long long)ldq, (long long)nq);
+  FASTRON_REQUIRE(((uintptr_t)qpos & 15) == 0, "qpos must be 16-byte aligned (float4 records)");
   FASTRON_REQUIRE(score || label, "score and label are both NULL");
   if (ns > 0) {
     FASTRON_REQUIRE(spos && alpha, "spos and alpha must be non-NULL when ns > 0");
     FASTRON_REQUIRE(lds >= ns, "lds (%lld) < ns (%lld)", (long long)lds, (long long)ns);
+    FASTRON_REQUIRE(((uintptr_t)spos & 15) == 0, "spos must be 16-byte aligned (float4 records)");
   }
   const size_t need = fastron_score_workspace_bytes(nq, ns, n_cp);
   if (workspace_bytes < need || (need > 0 && !workspace))
@@ -333,10 +335,13 @@ fastron_status fastron_score_packed(const float* qpos, int64_t nq, int64_t ldq, 
   FASTRON_REQUIRE(ldq >= nq, "ldq (%lld) < nq (%lld)", (long long)ldq, (long long)nq);
   FASTRON_REQUIRE(score || label, "score and label are both NULL");
   FASTRON_REQUIRE(ns == 0 || packed, "packed is NULL");
+  FASTRON_REQUIRE(((uintptr_t)qpos & 15) == 0, "qpos must be 16-byte aligned (float4 records)");
+  FASTRON_REQUIRE(ns == 0 || ((uintptr_t)packed & 255) == 0, "packed must be 256-byte aligned (fastron_model_pack)");
   const size_t need = fastron_score_packed_workspace_bytes(nq, ns, n_cp);
   if (workspace_bytes < need || (need > 0 && !workspace))
     return fail(FASTRON_ERR_WORKSPACE, "fastron_score_packed needs %zu workspace bytes, got %zu", need,
                 workspace_bytes);
+  FASTRON_REQUIRE(need == 0 || ((uintptr_t)workspace & 255) == 0, "workspace must be 256-byte aligned");
   FASTRON_VALIDATE(vcheck_f32(qpos, n_cp, 4 * nq, 4 * ldq, stream, "qpos"));
   return cuda_status(launch_score(reinterpret_cast<const float4*>(qpos), nq, ldq, static_cast<const float*>(packed), ns,
                                   n_cp, k.kind, kernel_scale(k), score, label, static_cast<double*>(workspace),
@@ -400,10 +405,13 @@ fastron_status fastron_score_packed_f64(const float* qpos, int64_t nq, int64_t l
   if (nq == 0) return FASTRON_OK;
   FASTRON_REQUIRE(qpos && score64 && ldq >= nq, "qpos and score64 must be non-NULL and ldq >= nq");
   FASTRON_REQUIRE(ns == 0 || packed, "packed is NULL");
+  FASTRON_REQUIRE(((uintptr_t)qpos & 15) == 0, "qpos must be 16-byte aligned (float4 records)");
+  FASTRON_REQUIRE(ns == 0 || ((uintptr_t)packed & 255) == 0, "packed must be 256-byte aligned (fastron_model_pack)");
   const size_t need = fastron_score_packed_workspace_bytes(nq, ns, n_cp);
   if (workspace_bytes < need || (need > 0 && !workspace))
     return fail(FASTRON_ERR_WORKSPACE, "fastron_score_packed_f64 needs %zu workspace bytes, got %zu", need,
                 workspace_bytes);
+  FASTRON_REQUIRE(need == 0 || ((uintptr_t)workspace & 255) == 0, "workspace must be 256-byte aligned");
   FASTRON_VALIDATE(vcheck_f32(qpos, n_cp, 4 * nq, 4 * ldq, stream, "qpos"));
   return cuda_status(launch_score(reinterpret_cast<const float4*>(qpos), nq, ldq, static_cast<const float*>(packed), ns,
                                   n_cp, k.kind, kernel_scale(k), nullptr, nullptr, static_cast<double*>(workspace),
