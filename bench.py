@@ -598,7 +598,7 @@ def run_ours(args):
         pass
     roof = {"bound": "alu", "pipe": "MUFU (SFU) ex2" if wl.kind == 0 else "MUFU (SFU) rcp",
             "achieved": achieved * 1e-12, "peak": peak * 1e-12, "unit": "Tops/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": "fastron_score_packed (score_kernel<8,kind,pos> + finalize)",
+            "traffic": traffic, "kernel": "fastron_score_packed (score_kernel<8,kind,pos> + finalize" + (")" if wl.kind == 0 else "; RQ: pass 1 fast term + pass 2 refinement of |f| < 0.5)"),
             "peak_source": f"{sms} SMs x {MUFU_PER_CLK_PER_SM} MUFU/clk x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
             "frac_at_run_clock": (achieved / (sms * MUFU_PER_CLK_PER_SM * clocks["sm_mhz"] * 1e6)
                                   if clocks.get("sm_mhz") else None),

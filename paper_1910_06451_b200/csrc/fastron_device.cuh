@@ -19,7 +19,8 @@
 namespace fastron {
 
 constexpr int kGaussian = 0;
-constexpr int kRQ = 1;
+constexpr int kRQ = 1;         // RQ, fast term (7 packed ops per pair): Gram, lazy columns, edges, scoring pass 1
+constexpr int kRQPrecise = 2;  // RQ, Newton-corrected term + offset lanes: the scores near the boundary
 
 // Support tile: TS supports per tile. Each support is MP/2 pair records of 8 floats
 // (x_m, x_m+1, y_m, y_m+1, z_m, z_m+1, 0, 0), pre-scaled, followed after the TS
@@ -104,13 +105,15 @@ __device__ __forceinline__ f2 term_pair(f2 ux, f2 uy, f2 uz, f2 vx, f2 vy, f2 vz
   return term_from_diffs<KIND>(sub2(ux, vx), sub2(uy, vy), sub2(uz, vz));
 }
 
-// RQ term evaluation (A/B knob; 1 = default):
-//  0: w = 1 + d2 as one FFMA chain seeded with 1, r = rcp(w), t = r^2 (7 packed ops per
-//     pair; w rounded three times at ulp(w) plus the rcp.approx error: ~3e-6 rms at the
-//     headline size, over the 1e-5 floor at |S| = 20,000 — DESIGN.md §5)
-//  1: s = d2 first (rounded at ulp(d2)), w = 1 + s, r0 = rcp(w), then one Newton step
-//     against the UNROUNDED 1 + s: e = (1 - r0) - r0 s, r = r0 (1 + e). The residual
-//     removes both the rounding of w and the rcp.approx error (11 packed ops per pair).
+// RQ term evaluation. kRQ (fast): w = 1 + d2 as one FFMA chain seeded with 1, r = rcp(w),
+// t = r^2 (7 packed ops per pair; w rounded three times at ulp(w): ~3e-6 rms at the
+// headline size — ample for the Gram (relative 1e-4) and for scores away from 0).
+// kRQPrecise: s = d2 first (rounded at ulp(d2)), w = 1 + s, r0 = rcp(w), then one Newton
+// step against the UNROUNDED 1 + s: e = (1 - r0) - r0 s, r = r0 (1 + e); the residual
+// removes both the rounding of w and the rcp.approx error (11 packed ops per pair,
+// ~1.4e-6 rms with the offset lanes). The scoring kernels use it for the
+// queries whose fast score lies within kRefineTau of 0 (score.cu, pass 2) and for small
+// batches. FASTRON_RQ_NEWTON=0 makes kRQPrecise the fast term (A/B).
 #ifndef FASTRON_RQ_NEWTON
 #define FASTRON_RQ_NEWTON 1
 #endif
@@ -118,11 +121,10 @@ __device__ __forceinline__ f2 term_pair(f2 ux, f2 uy, f2 uz, f2 vx, f2 vy, f2 vz
 // acc (+)= the terms of control points (m, m+1): the per-lane running sum over the pairs
 // p = 0, 1, ... (first: p == 0, the lane starts from `init`). Every kernel accumulates
 // through this one function, so the Gram, the scores and the lazy columns stay
-// bit-identical (the scoring kernels start the RQ lanes from -offset, see rq_lane_offset).
-// Gaussian: t = 2^-d2 as above, then acc + t.
-// RQ (FASTRON_RQ_NEWTON, see above): the square of r = (1 + d2)^-1 rides in the
-// accumulating FFMA2. The MUFU takes the source negation for free, so the Newton step runs
-// on nr0 = rcp(-w) = -r0 without separate negations:
+// bit-identical for the same KIND.
+// Gaussian: t = 2^-d2 as above, then acc + t. RQ: the square of r = (1 + d2)^-1 rides in
+// the accumulating FFMA2. kRQPrecise: the MUFU takes the source negation for free, so the
+// Newton step runs on nr0 = rcp(-w) = -r0 without separate negations:
 //   u = 1 + nr0 (= 1 - r0, exact for r0 >= 1/2), e = fma(nr0, s, u), nr = fma(nr0, e, nr0)
 //   (= -r), acc = fma(nr, nr, acc).
 template <int KIND>
@@ -130,16 +132,8 @@ __device__ __forceinline__ void accum_term(f2& acc, f2 dx, f2 dy, f2 dz, bool fi
   if (KIND == kGaussian) {
     const f2 t = term_from_diffs<KIND>(dx, dy, dz);
     acc = first ? (init ? add2(init, t) : t) : add2(acc, t);
-  } else {
+  } else if (KIND == kRQPrecise && FASTRON_RQ_NEWTON) {
     const f2 one = pk(1.0f, 1.0f);
-#if FASTRON_RQ_NEWTON == 2
-    f2 s = mul2(dx, dx);  // s-form without the Newton step (A/B only)
-    s = fma2(dy, dy, s);
-    s = fma2(dz, dz, s);
-    const f2 w = add2(s, one);
-    const f2 r = pk(rcp_approx(lo(w)), rcp_approx(hi(w)));
-    acc = fma2(r, r, first ? init : acc);
-#elif FASTRON_RQ_NEWTON
     f2 s = mul2(dx, dx);
     s = fma2(dy, dy, s);
     s = fma2(dz, dz, s);
@@ -149,28 +143,28 @@ __device__ __forceinline__ void accum_term(f2& acc, f2 dx, f2 dy, f2 dz, bool fi
     const f2 e = fma2(nr0, s, u);
     const f2 nr = fma2(nr0, e, nr0);
     acc = fma2(nr, nr, first ? init : acc);
-#else
+  } else {
+    const f2 one = pk(1.0f, 1.0f);
     f2 w = fma2(dx, dx, one);
     w = fma2(dy, dy, w);
     w = fma2(dz, dz, w);
     const f2 r = pk(rcp_approx(lo(w)), rcp_approx(hi(w)));
     acc = first ? (init ? fma2(r, r, init) : mul2(r, r)) : fma2(r, r, acc);
-#endif
   }
 }
 
-// Lane offset of the scoring kernels' RQ sums (A/B knob FASTRON_RQ_OFFSET, 1 = default).
-// Under RQ every support contributes (k >= 0.14 on these arms), and each fp32 lane sums
-// NP terms of mean ~0.35 (headline): the rounding of the running sum at ulp(~1.4) was
-// ~1.6e-6 rms of the headline score error. Starting each lane from -NP/4 keeps the running
-// sums near 0; the scoring kernels add 2 * (NP/4) * sum(alpha) back in fp64 (exact), so
-// the value is unchanged and only the rounding shrinks.
+// Lane offset of the scoring kernels' precise RQ sums (A/B knob FASTRON_RQ_OFFSET,
+// 1 = default). Under RQ every support contributes (k >= 0.14 on these arms), and each fp32
+// lane sums NP terms of mean ~0.35 (headline): the rounding of the running sum at
+// ulp(~1.4) was ~1.6e-6 rms of the headline score error. Starting each lane from -NP/4
+// keeps the running sums near 0; the scoring kernels add 2 * (NP/4) * sum(alpha) back in
+// fp64 (exact), so the value is unchanged and only the rounding shrinks.
 #ifndef FASTRON_RQ_OFFSET
 #define FASTRON_RQ_OFFSET 1
 #endif
 template <int KIND, int NP>
 __host__ __device__ constexpr float rq_lane_offset() {
-  return (KIND == kRQ && FASTRON_RQ_OFFSET) ? 0.25f * (float)NP : 0.0f;
+  return (KIND == kRQPrecise && FASTRON_RQ_OFFSET) ? 0.25f * (float)NP : 0.0f;
 }
 
 // Sum over the M control points of one (query, support) pair, in the fixed order

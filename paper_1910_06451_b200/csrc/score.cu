@@ -143,7 +143,28 @@ struct ScoreArgs {
   int64_t plan_nq;  // host only: batch size the split count is planned for (0: nq)
   const float* qcfg;  // small fused query: configurations [nq][ldqc] (FK in the kernel)
   int64_t ldqc;
+  // RQ refinement: pass 1 (fast term) appends the queries whose score lies
+  // within refine_tau of 0 to refine_list; pass 2 (precise term) scores exactly those:
+  // query vq of pass 2 is query qidx[vq] of the batch, for vq < *qcount
+  int32_t* refine_list;
+  int32_t* refine_count;
+  double refine_tau;
+  const int32_t* qidx;
+  const int32_t* qcount;
 };
+
+// |f| below which a fast RQ score is recomputed with the precise term. The fast term's
+// error at the headline size is rms 3.0e-6, max ~1.1e-5 (5.5 sigma over 1M queries ~1.7e-5);
+// at |f| >= 0.5 the tolerance is >= 5e-5, a 3x margin, and ~0.9 % of the headline's
+// queries fall below it.
+constexpr double kRefineTau = 0.5;
+
+__device__ __forceinline__ void maybe_refine(const ScoreArgs& A, int64_t vq, double fm) {
+  if (A.refine_list && fabs(fm) < A.refine_tau) A.refine_list[atomicAdd(A.refine_count, 1)] = (int32_t)vq;
+}
+
+// pass 2: the batch index of (virtual) query vq
+__device__ __forceinline__ int64_t batch_query(const ScoreArgs& A, int64_t vq) { return A.qidx ? A.qidx[vq] : vq; }
 
 // Final write of one query's fp64 sum: 1/denom, fp64 / fp32 score, label (R8).
 __device__ __forceinline__ void write_score(const ScoreArgs& A, int64_t vq, double f) {
@@ -239,8 +260,8 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
   const int64_t qb = blockIdx.x / A.n_splits;
   const int split = blockIdx.x % A.n_splits;
   const int64_t q_base = qb * (int64_t)(kNT * QT);
-  const int64_t nq_live = MODE == MODE_EDGE ? edge_active_queries(A) : A.nq;
-  if (q_base >= nq_live) return;  // uniform: whole CTA idle (edge rounds sized for the worst case)
+  const int64_t nq_live = MODE == MODE_EDGE ? edge_active_queries(A) : (A.qcount ? (int64_t)*A.qcount : A.nq);
+  if (q_base >= nq_live) return;  // uniform: whole CTA idle (edge rounds / refinement: worst-case grids)
 
   const int64_t t0 = (int64_t)split * A.tiles_per_split;
   const int64_t t1 = min(t0 + (int64_t)A.tiles_per_split, A.n_tiles);
@@ -271,9 +292,11 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
       // positions of the query (MODE_EDGE: of the interpolated configuration, written by
       // edge_fk_kernel for this round)
 #pragma unroll
+      const int64_t bq = batch_query(A, vq);
+#pragma unroll
       for (int m = 0; m < MP; ++m) {
         if (m < A.M) {
-          const float4 v = __ldg(A.qpos + (int64_t)m * A.ldq + vq);
+          const float4 v = __ldg(A.qpos + (int64_t)m * A.ldq + bq);
           px[m] = v.x; py[m] = v.y; pz[m] = v.z;
         }
       }
@@ -365,7 +388,7 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
 #pragma unroll
       for (int j = 0; j < QT; ++j) {
 #if FASTRON_ACC_SPLIT
-        if (KIND == kRQ && MODE != MODE_JOINT) {  // offset lanes can be negative
+        if (KIND == kRQPrecise && MODE != MODE_JOINT) {  // offset lanes can be negative
           f[j] = fma(a, rq_lane_to_f64(lo(acc[j])), f[j]);
           f[j] = fma(a, rq_lane_to_f64(hi(acc[j])), f[j]);
         } else {
@@ -396,11 +419,13 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
     if (A.n_splits > 1) {
       if (vq < nq_live) A.partial[(int64_t)split * A.nq + vq] = f[j];
     } else if (MODE == MODE_POS || MODE == MODE_JOINT) {
-      if (vq < A.nq) {
+      if (vq < nq_live) {
         const double fm = f[j] / A.denom;
-        if (A.score64) A.score64[vq] = fm;
-        if (A.score) A.score[vq] = (float)fm;
-        if (A.label) A.label[vq] = fm > 0.0 ? 1 : -1;
+        const int64_t bq = batch_query(A, vq);
+        if (A.score64) A.score64[bq] = fm;
+        if (A.score) A.score[bq] = (float)fm;
+        if (A.label) A.label[bq] = fm > 0.0 ? 1 : -1;
+        maybe_refine(A, vq, fm);
       }
     } else {
       edge_vote(A, vq, f[j] / A.denom);
@@ -412,10 +437,10 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
 template <int MODE>
 __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ ScoreArgs A) {
   const int64_t vq = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nq_live = MODE == MODE_EDGE ? edge_active_queries(A) : A.nq;
+  const int64_t nq_live = MODE == MODE_EDGE ? edge_active_queries(A) : (A.qcount ? (int64_t)*A.qcount : A.nq);
   if (MODE == MODE_EDGE) {
     if ((vq & ~(int64_t)31) >= nq_live) return;  // warp-uniform
-  } else if (vq >= A.nq) {
+  } else if (vq >= nq_live) {
     return;
   }
   double f = 0.0;
@@ -423,9 +448,11 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ S
     for (int s = 0; s < A.n_splits; ++s) f += A.partial[(int64_t)s * A.nq + vq];
   const double fm = f / A.denom;
   if (MODE == MODE_POS || MODE == MODE_JOINT) {
-    if (A.score64) A.score64[vq] = fm;
-    if (A.score) A.score[vq] = (float)fm;
-    if (A.label) A.label[vq] = fm > 0.0 ? 1 : -1;
+    const int64_t bq = batch_query(A, vq);
+    if (A.score64) A.score64[bq] = fm;
+    if (A.score) A.score[bq] = (float)fm;
+    if (A.label) A.label[bq] = fm > 0.0 ? 1 : -1;
+    maybe_refine(A, vq, fm);
   } else {
     edge_vote(A, vq, fm);
   }
@@ -442,8 +469,8 @@ __global__ void __launch_bounds__(256) finalize_grouped_kernel(const __grid_cons
   __shared__ double part[8][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t vq = (int64_t)blockIdx.x * 32 + lane;
-  const int64_t nq_live = MODE == MODE_EDGE ? edge_active_queries(A) : A.nq;
-  if (MODE == MODE_EDGE && (int64_t)blockIdx.x * 32 >= nq_live) return;  // CTA-uniform
+  const int64_t nq_live = MODE == MODE_EDGE ? edge_active_queries(A) : (A.qcount ? (int64_t)*A.qcount : A.nq);
+  if ((int64_t)blockIdx.x * 32 >= nq_live) return;  // CTA-uniform
   const int per = (A.n_splits + 7) / 8;
   const int s0 = w * per, s1 = min(A.n_splits, s0 + per);
   double f = 0.0;
@@ -457,10 +484,12 @@ __global__ void __launch_bounds__(256) finalize_grouped_kernel(const __grid_cons
   for (int g = 1; g < 8; ++g) f += part[g][lane];
   const double fm = f / A.denom;
   if (MODE == MODE_POS || MODE == MODE_JOINT) {
-    if (vq < A.nq) {
-      if (A.score64) A.score64[vq] = fm;
-      if (A.score) A.score[vq] = (float)fm;
-      if (A.label) A.label[vq] = fm > 0.0 ? 1 : -1;
+    if (vq < nq_live) {
+      const int64_t bq = batch_query(A, vq);
+      if (A.score64) A.score64[bq] = fm;
+      if (A.score) A.score[bq] = (float)fm;
+      if (A.label) A.label[bq] = fm > 0.0 ? 1 : -1;
+      maybe_refine(A, vq, fm);
     }
   } else {
     edge_vote(A, vq, fm);
@@ -559,7 +588,7 @@ __global__ void __launch_bounds__(kSmallNT) score_small_kernel(const __grid_cons
         for (int p = 0; p < NP; ++p)
           accum_term<KIND>(acc, sub2(sq[q][p][0], vx[p]), sub2(sq[q][p][1], vy[p]), sub2(sq[q][p][2], vz[p]), p == 0,
                            lane0);
-        if (KIND == kRQ) {  // offset lanes can be negative
+        if (KIND == kRQPrecise) {  // offset lanes can be negative
           f[q] = fma(a, rq_lane_to_f64(lo(acc)), f[q]);
           f[q] = fma(a, rq_lane_to_f64(hi(acc)), f[q]);
         } else {
@@ -657,11 +686,17 @@ int score_max_splits(int64_t nq, int64_t ns, int M) {
   return (int)(cap < 1 ? 1 : cap);
 }
 
-size_t score_partial_bytes(int64_t nq, int64_t ns, int M) {
+// The partial region: split partials (or the small kernel's CTA partials), then the RQ
+// refinement list (nq int32) and its counter.
+static size_t score_partial_core_bytes(int64_t nq, int64_t ns, int M) {
   const int s = score_max_splits(nq, ns, M);
   const size_t tiles = s > 1 ? (size_t)s * (size_t)nq * sizeof(double) : 0;
   const size_t small = (nq > 0 && nq <= kSmallQ && M <= 16) ? score_small_bytes() : 0;
-  return tiles > small ? tiles : small;
+  return ((tiles > small ? tiles : small) + 255) & ~(size_t)255;
+}
+
+size_t score_partial_bytes(int64_t nq, int64_t ns, int M) {
+  return score_partial_core_bytes(nq, ns, M) + (((size_t)(nq > 0 ? nq : 0) * 4 + 255) & ~(size_t)255) + 256;
 }
 
 template <int MP, int KIND, int MODE>
@@ -762,8 +797,10 @@ static cudaError_t run_score(const ScoreArgs& base, const FkParams& P, int64_t n
 template <int MODE>
 static cudaError_t dispatch(const ScoreArgs& A, const FkParams& P, int64_t nq, int64_t ns, int kind, cudaStream_t st) {
   const int MP = padded_m(A.M);
+  // kind: kGaussian, kRQ (fast) or, for MODE_POS only, kRQPrecise (refinement pass 2)
 #define FASTRON_CASE(mp)                                                                   \
   case mp:                                                                                 \
+    if (MODE == MODE_POS && kind == kRQPrecise) return run_score<mp, kRQPrecise, MODE_POS>(A, P, nq, ns, st); \
     return kind == kGaussian ? run_score<mp, kGaussian, MODE>(A, P, nq, ns, st)            \
                              : run_score<mp, kRQ, MODE>(A, P, nq, ns, st);
   switch (MP) {
@@ -866,7 +903,7 @@ cudaError_t launch_score(const float4* qpos, int64_t nq, int64_t ldq, const floa
     switch (padded_m(M)) {
 #define FASTRON_SCASE(mp)                                                                            \
   case mp:                                                                                           \
-    return kind == kGaussian ? run_score_small<mp, kGaussian>(A, ns, st) : run_score_small<mp, kRQ>(A, ns, st);
+    return kind == kGaussian ? run_score_small<mp, kGaussian>(A, ns, st) : run_score_small<mp, kRQPrecise>(A, ns, st);
       FASTRON_SCASE(2)
       FASTRON_SCASE(4)
       FASTRON_SCASE(6)
@@ -879,6 +916,29 @@ cudaError_t launch_score(const float4* qpos, int64_t nq, int64_t ldq, const floa
       default:
         break;
     }
+  }
+  if (kind == kRQ && ns > 0 && partial) {
+    // RQ in two passes: the fast term for every query, then the precise
+    // (Newton + offset lanes) term for the queries whose fast score lies within
+    // kRefineTau of 0 — found by pass 1's epilogue, scored by pass 2 over a worst-case grid
+    // whose CTAs beyond the device-side count exit at once (no host synchronisation)
+    // (laid out for this call's nq: a chunk of a larger batch gets a region sized for the
+    // chunk capacity, and core(nq) + list(nq) is monotone in nq)
+    char* region = reinterpret_cast<char*>(partial) + score_partial_core_bytes(nq, ns, M);
+    int32_t* list = reinterpret_cast<int32_t*>(region);
+    int32_t* count = reinterpret_cast<int32_t*>(region + (((size_t)nq * 4 + 255) & ~(size_t)255));
+    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(int32_t), st);
+    if (e != cudaSuccess) return e;
+    ScoreArgs A1 = A;
+    A1.refine_list = list;
+    A1.refine_count = count;
+    A1.refine_tau = kRefineTau;
+    e = dispatch<MODE_POS>(A1, P, nq, ns, kRQ, st);
+    if (e != cudaSuccess) return e;
+    ScoreArgs A2 = A;
+    A2.qidx = list;
+    A2.qcount = count;
+    return dispatch<MODE_POS>(A2, P, nq, ns, kRQPrecise, st);
   }
   return dispatch<MODE_POS>(A, P, nq, ns, kind, st);
 }
@@ -903,7 +963,7 @@ cudaError_t launch_query_small(const FkParams& P, const float* q, int64_t nq, in
 #define FASTRON_QCASE(mp)                                                                   \
   case mp:                                                                                  \
     return kind == kGaussian ? run_score_small<mp, kGaussian, true>(A, ns, st, P)           \
-                             : run_score_small<mp, kRQ, true>(A, ns, st, P);
+                             : run_score_small<mp, kRQPrecise, true>(A, ns, st, P);
     FASTRON_QCASE(2)
     FASTRON_QCASE(4)
     FASTRON_QCASE(6)
