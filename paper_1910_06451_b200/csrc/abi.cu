@@ -23,6 +23,17 @@ namespace fastron {
 
 std::atomic<int64_t> g_launches{0};
 
+// Off by default: measured A/B on the B200 (same box, bench --rows): headline 40.13 ->
+// 40.48 ms with PDL, cfg1 graph replay 24.6 -> 28.7 us, small batches 0-2 us faster
+// (DESIGN.md §6). FASTRON_PDL=1 turns it on.
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("FASTRON_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 // Per-device properties, queried once. The fast path is a lock-free acquire load of the
 // device's ready flag (the mutex only serialises the first query per device).
 const DeviceInfo& device_info() {

@@ -20,6 +20,8 @@ constexpr int kFkCpt = FASTRON_FK_CPT;  // configurations per thread
 __global__ void __launch_bounds__(kFkThreads) fk_kernel(const __grid_constant__ FkParams P, const float* __restrict__ q,
                                                         int64_t n, int64_t ldq, float4* __restrict__ pos,
                                                         int64_t ldpos) {
+  pdl_trigger();
+  pdl_wait();
   if (kFkCpt == 1) {
     const int64_t k = (int64_t)blockIdx.x * kFkThreads + threadIdx.x;
     if (k >= n) return;
@@ -54,9 +56,8 @@ cudaError_t launch_fk(const FkParams& P, const float* q, int64_t n, int64_t ldq,
                       cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int64_t blocks = (n + kFkThreads * kFkCpt - 1) / (kFkThreads * kFkCpt);
-  fk_kernel<<<(unsigned)blocks, kFkThreads, 0, st>>>(P, q, n, ldq, pos, ldpos);
   g_launches.fetch_add(1);
-  return cudaGetLastError();
+  return launch_pdl(fk_kernel, dim3((unsigned)blocks), dim3(kFkThreads), 0, st, P, q, n, ldq, pos, ldpos);
 }
 
 }  // namespace fastron

@@ -27,6 +27,31 @@ inline int device_slot() {
   return d >= 0 && d < kMaxDevices ? d : 0;
 }
 
+// Programmatic dependent launch (PDL): the query-path kernels (FK, pack, scoring, finalize,
+// edge FK, small batches) are launched with programmatic stream serialisation, so a kernel
+// is scheduled while its predecessor drains; each one calls pdl_wait() (griddepcontrol.wait:
+// the predecessor has completed and its memory is visible) before its first global-memory
+// access and pdl_trigger() at its start. Off by default (measured slower on the headline
+// and on cfg1 graph replays); FASTRON_PDL=1 (env) turns it on.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<Args&&>(args)...);
+}
+
 // K1: control-point positions, float4 [M][ldpos]
 cudaError_t launch_fk(const FkParams& P, const float* q, int64_t n, int64_t ldq, float4* pos, int64_t ldpos,
                       cudaStream_t st);

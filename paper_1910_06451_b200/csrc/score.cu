@@ -72,6 +72,8 @@ int score_queries_per_cta(int M) { return kNT * qt_for(padded_m(M)); }
 // ---------------------------------------------------------------------------------
 __global__ void pack_kernel(const float4* __restrict__ spos, int64_t lds, const float* __restrict__ alpha, int64_t ns,
                             int M, int MP, float scale, float pad, float* __restrict__ packed, int64_t n_slots) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_slots) return;
   const int64_t tile = i / kTileSupports;
@@ -98,10 +100,9 @@ cudaError_t launch_pack(const float4* spos, int64_t lds, const float* alpha, int
   const int64_t slots = n_support_tiles(ns) * kTileSupports;
   if (slots == 0) return cudaSuccess;
   const int threads = 256;
-  pack_kernel<<<(unsigned)((slots + threads - 1) / threads), threads, 0, st>>>(
-      spos, lds, alpha, ns, M, padded_m(M), scale, joint ? 0.0f : kPadCoord, packed, slots);
   g_launches.fetch_add(1);
-  return cudaGetLastError();
+  return launch_pdl(pack_kernel, dim3((unsigned)((slots + threads - 1) / threads)), dim3(threads), 0, st, spos, lds,
+                    alpha, ns, M, padded_m(M), scale, joint ? 0.0f : kPadCoord, packed, slots);
 }
 
 // ---------------------------------------------------------------------------------
@@ -215,6 +216,8 @@ __device__ __forceinline__ void edge_vote(const ScoreArgs& A, int64_t vq, double
 // n_interp get zeros (they never vote). Computed once instead of in every support split.
 __global__ void __launch_bounds__(256) edge_fk_kernel(const __grid_constant__ ScoreArgs A,
                                                       const __grid_constant__ FkParams P, float4* __restrict__ pos) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t vq = (int64_t)blockIdx.x * 256 + threadIdx.x;
   if (vq >= edge_active_queries(A)) return;
   const int64_t slot = vq >> 5;
@@ -257,6 +260,8 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
   float* stages = reinterpret_cast<float*>(smem_raw + 128);
 
   const int tid = threadIdx.x;
+  pdl_trigger();
+  pdl_wait();  // before any global access (the counts, the packed tiles, the positions)
   const int64_t qb = blockIdx.x / A.n_splits;
   const int split = blockIdx.x % A.n_splits;
   const int64_t q_base = qb * (int64_t)(kNT * QT);
@@ -291,7 +296,6 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
     if (vq < nq_live) {
       // positions of the query (MODE_EDGE: of the interpolated configuration, written by
       // edge_fk_kernel for this round)
-#pragma unroll
       const int64_t bq = batch_query(A, vq);
 #pragma unroll
       for (int m = 0; m < MP; ++m) {
@@ -436,6 +440,8 @@ __global__ void __launch_bounds__(kNT) score_kernel(const __grid_constant__ Scor
 // Fixed-order reduction of the split partials (deterministic), then 1/M, score, label / vote.
 template <int MODE>
 __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ ScoreArgs A) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t vq = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nq_live = MODE == MODE_EDGE ? edge_active_queries(A) : (A.qcount ? (int64_t)*A.qcount : A.nq);
   if (MODE == MODE_EDGE) {
@@ -467,6 +473,8 @@ constexpr int kSeqSplits = 16;
 template <int MODE>
 __global__ void __launch_bounds__(256) finalize_grouped_kernel(const __grid_constant__ ScoreArgs A) {
   __shared__ double part[8][32];
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t vq = (int64_t)blockIdx.x * 32 + lane;
   const int64_t nq_live = MODE == MODE_EDGE ? edge_active_queries(A) : (A.qcount ? (int64_t)*A.qcount : A.nq);
@@ -524,6 +532,8 @@ __global__ void __launch_bounds__(kSmallNT) score_small_kernel(const __grid_cons
   __shared__ float s_pos[FUSED_FK ? kSmallQ : 1][FUSED_FK ? MP : 1][3];
   __shared__ int s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  pdl_trigger();
+  pdl_wait();
   const int nq = (int)A.nq;
   if (FUSED_FK) {
     // the thread's first support record travels to L1 while the D-H chains run
@@ -649,9 +659,9 @@ static cudaError_t run_score_small(const ScoreArgs& A, int64_t ns, cudaStream_t 
   unsigned int* ticket = reinterpret_cast<unsigned int*>(A.partial + (int64_t)device_info().sms * kSmallQ);
   cudaError_t e = cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st);
   if (e != cudaSuccess) return e;
-  score_small_kernel<MP, KIND, FUSED_FK><<<(unsigned)grid, kSmallNT, 0, st>>>(A, P, ns, ticket);
   g_launches.fetch_add(1);
-  return cudaGetLastError();
+  return launch_pdl(score_small_kernel<MP, KIND, FUSED_FK>, dim3((unsigned)grid), dim3(kSmallNT), 0, st, A, P, ns,
+                    ticket);
 }
 
 size_t score_small_bytes() { return (size_t)device_info().sms * kSmallQ * sizeof(double) + 256; }
@@ -777,21 +787,22 @@ static cudaError_t run_score(const ScoreArgs& base, const FkParams& P, int64_t n
       cudaFuncSetAttribute(score_kernel<MP, KIND, MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr[dev].store(1);
     }
-    score_kernel<MP, KIND, MODE, 1><<<(unsigned)grid, kNT, smem, st>>>(A, P);
+  }
+  cudaError_t e;
+  if (one_q) {
+    e = launch_pdl(score_kernel<MP, KIND, MODE, 1>, dim3((unsigned)grid), dim3(kNT), smem, st, A, P);
   } else {
-    score_kernel<MP, KIND, MODE><<<(unsigned)grid, kNT, smem, st>>>(A, P);
+    e = launch_pdl(score_kernel<MP, KIND, MODE>, dim3((unsigned)grid), dim3(kNT), smem, st, A, P);
   }
   g_launches.fetch_add(1);
-  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || plan.n_splits == 1) return e;
   if (plan.n_splits > kSeqSplits) {
-    finalize_grouped_kernel<MODE><<<(unsigned)((nq + 31) / 32), 256, 0, st>>>(A);
+    e = launch_pdl(finalize_grouped_kernel<MODE>, dim3((unsigned)((nq + 31) / 32)), dim3(256), 0, st, A);
   } else {
-    const int64_t fgrid = (nq + 255) / 256;
-    finalize_kernel<MODE><<<(unsigned)fgrid, 256, 0, st>>>(A);
+    e = launch_pdl(finalize_kernel<MODE>, dim3((unsigned)((nq + 255) / 256)), dim3(256), 0, st, A);
   }
   g_launches.fetch_add(1);
-  return cudaGetLastError();
+  return e;
 }
 
 template <int MODE>
@@ -1001,9 +1012,8 @@ cudaError_t launch_edge_round(const FkParams& P, const EdgeRound& R, const float
   A.in_collision = R.in_collision;
   A.hit_index = R.hit_index;
   A.denom = (double)M;
-  edge_fk_kernel<<<(unsigned)((A.nq + 255) / 256), 256, 0, st>>>(A, P, pos);
   g_launches.fetch_add(1);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(edge_fk_kernel, dim3((unsigned)((A.nq + 255) / 256)), dim3(256), 0, st, A, P, pos);
   if (e != cudaSuccess) return e;
   return dispatch<MODE_EDGE>(A, P, A.nq, ns, kind, st);
 }
