@@ -436,6 +436,12 @@ def _time_rows(fb, torch, kind):
                                               workspace=qws_)
                 lat[f"S{ns}_q{nq}"]["query_stream_us"] = timed(fq, 200) * 1e3
                 lat[f"S{ns}_q{nq}"]["query_graph_us"] = graphed(fq, 200) * 1e3
+            # fastron_query_packed: the planner's call (model packed once; one launch at nq <= 32)
+            pws = torch.empty(max(256, fb.load_library().fastron_query_packed_workspace_bytes(nq, ns, 8, 7)),
+                              dtype=torch.uint8, device="cuda")
+            fqp = lambda: fb.fastron_query_packed(robot_c, qs, mdl, sc, lb, workspace=pws)
+            lat[f"S{ns}_q{nq}"]["query_packed_stream_us"] = timed(fqp, 200) * 1e3
+            lat[f"S{ns}_q{nq}"]["query_packed_graph_us"] = graphed(fqp, 200) * 1e3
     rows["small_batch_latency"] = lat
     # cfg4: 10k edges x 64 points, 3k supports, early exit
     ew = W.edge_workload()

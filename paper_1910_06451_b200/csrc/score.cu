@@ -516,6 +516,7 @@ __global__ void __launch_bounds__(256) finalize_grouped_kernel(const __grid_cons
 constexpr int kSmallQ = 32;
 constexpr int kSmallNT = 256;
 constexpr int kSmallChunk = 32;  // CTA partials fetched per round by the last CTA
+constexpr int64_t kSmallOneCtaTerms = 32768;  // nq * ns * M up to which one CTA scores the batch
 
 // FUSED_FK: the queries arrive as configurations and thread q runs the D-H chain of
 // query q (fk_chain, the FK kernel's arithmetic and rounding: the same positions), so a
@@ -626,8 +627,13 @@ __global__ void __launch_bounds__(kSmallNT) score_small_kernel(const __grid_cons
     double v = 0.0;
 #pragma unroll
     for (int w = 0; w < kSmallNT / 32; ++w) v += s_red[w][tid];
+    if (gridDim.x == 1) {
+      write_score(A, tid, 0.0 + v);  // the multi-CTA path's sum over one partial, same bits
+      return;
+    }
     A.partial[(int64_t)blockIdx.x * kSmallQ + tid] = v;
   }
+  if (gridDim.x == 1) return;
   __threadfence();
   __syncthreads();
   if (tid == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
@@ -653,12 +659,17 @@ __global__ void __launch_bounds__(kSmallNT) score_small_kernel(const __grid_cons
 
 template <int MP, int KIND, bool FUSED_FK = false>
 static cudaError_t run_score_small(const ScoreArgs& A, int64_t ns, cudaStream_t st, const FkParams& P = FkParams{}) {
-  const int64_t want = (ns + kSmallNT - 1) / kSmallNT;
+  // one CTA when the whole batch is a few thousand terms (a planner's single query against
+  // a Table-I-size model): no cross-CTA partials, ticket or memset
+  const bool one_cta = A.nq * ns * (int64_t)A.M <= kSmallOneCtaTerms;
+  const int64_t want = one_cta ? 1 : (ns + kSmallNT - 1) / kSmallNT;
   const int64_t grid = want < 1 ? 1 : (want > device_info().sms ? device_info().sms : want);
   // partials: [grid][kSmallQ] doubles; the ticket counter follows them
   unsigned int* ticket = reinterpret_cast<unsigned int*>(A.partial + (int64_t)device_info().sms * kSmallQ);
-  cudaError_t e = cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st);
-  if (e != cudaSuccess) return e;
+  if (grid > 1) {
+    cudaError_t e = cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st);
+    if (e != cudaSuccess) return e;
+  }
   g_launches.fetch_add(1);
   return launch_pdl(score_small_kernel<MP, KIND, FUSED_FK>, dim3((unsigned)grid), dim3(kSmallNT), 0, st, A, P, ns,
                     ticket);

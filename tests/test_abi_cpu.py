@@ -147,3 +147,46 @@ def test_validation_switch():
     fb.set_validation(False)
     assert not fb.validation()
     fb.set_validation(before)
+
+
+def test_round2_entry_points_argument_errors():
+    """The round-2 calls reject bad arguments before any CUDA work: n_cp mismatches,
+    misaligned float4/double4/packed pointers, short workspaces, unsupported n_cp."""
+    L = fb.load_library()
+    r = _robot()
+    k = fb.fastron_kernel(0, 5.0)
+    A = 1 << 20  # an aligned, never dereferenced address
+    # fastron_query_packed: n_cp must match the robot; packed 256-byte aligned
+    st, msg = _err(L.fastron_query_packed(ctypes.byref(r), A, 10, 7, A, 100, 16, k, A, None, A, 1 << 20, None))
+    assert st == fb.FASTRON_ERR_INVALID_ARG and "n_cp" in msg
+    assert L.fastron_query_packed(ctypes.byref(r), None, 0, 7, None, 0, 8, k, None, None, None, 0, None) == fb.FASTRON_OK
+    # fastron_edge_check_packed
+    st, msg = _err(L.fastron_edge_check_packed(ctypes.byref(r), A, A, 10, 7, 64, A, 100, 4, k, A, None, A, 1 << 20, None))
+    assert st == fb.FASTRON_ERR_INVALID_ARG and "n_cp" in msg
+    st, msg = _err(L.fastron_edge_check_packed(ctypes.byref(r), A, A, 10, 7, 64, A + 16, 100, 8, k, A, None, A,
+                                               1 << 24, None))
+    assert st == fb.FASTRON_ERR_INVALID_ARG and "aligned" in msg
+    assert L.fastron_edge_check_packed(ctypes.byref(r), A, A, 10, 7, 0, A, 100, 8, k, A, None, A, 1 << 24,
+                                       None) == fb.FASTRON_ERR_INVALID_ARG  # n_interp < 1
+    # fastron_score_packed: packed and qpos alignment
+    st, msg = _err(L.fastron_score_packed(A, 10, 10, A + 16, 100, 8, k, A, None, A, 1 << 24, None))
+    assert st == fb.FASTRON_ERR_INVALID_ARG and "packed" in msg
+    st, msg = _err(L.fastron_score_packed(A + 8, 10, 10, A, 100, 8, k, A, None, A, 1 << 24, None))
+    assert st == fb.FASTRON_ERR_INVALID_ARG and "qpos" in msg
+    # fastron_kernel_matvec_lazy: n_cp range, workspace size and alignment
+    assert L.fastron_kernel_matvec_lazy(A, 10, 10, 0, k, A, A, A, 1 << 20, None) == fb.FASTRON_ERR_INVALID_ARG
+    st, msg = _err(L.fastron_kernel_matvec_lazy(A, 1000, 1000, 8, k, A, A, A, 16, None))
+    assert st == fb.FASTRON_ERR_WORKSPACE
+    assert L.fastron_kernel_matvec_lazy(A + 8, 10, 10, 8, k, A, A, A, 1 << 20, None) == fb.FASTRON_ERR_INVALID_ARG
+    # fastron_fk64 / fastron_score_precise: double4 alignment, n_cp <= 16
+    assert L.fastron_fk64(ctypes.byref(r), A, 10, 7, A + 16, 10, None) == fb.FASTRON_ERR_INVALID_ARG
+    st, msg = _err(L.fastron_score_precise(A, 10, 10, A, A, 5, 5, 17, k, A, None, None))
+    assert st == fb.FASTRON_ERR_UNSUPPORTED and "n_cp" in msg
+    assert L.fastron_score_precise(A + 16, 10, 10, A, A, 5, 5, 8, k, A, None, None) == fb.FASTRON_ERR_INVALID_ARG
+    assert L.fastron_score_precise(A, 10, 10, A, A, 5, 4, 8, k, A, None, None) == fb.FASTRON_ERR_INVALID_ARG
+    assert L.fastron_score_precise(None, 0, 0, None, None, 0, 0, 8, k, None, None, None) == fb.FASTRON_OK
+    # workspace sizes: host-only queries
+    assert L.fastron_query_packed_workspace_bytes(1 << 20, 20_000, 8, 7) > 0
+    assert L.fastron_edge_packed_workspace_bytes(10_000, 3000, 8) > 0
+    assert L.fastron_kernel_matvec_lazy_workspace_bytes(20_000, 16) > 0
+    assert L.fastron_train_lazy_max_n(16) == 32_768
