@@ -1,9 +1,20 @@
 // gram.cu — K3, the FK-kernel Gram matrix K_ij = K_FK(X_i, X_j) (
 // Algorithm 1's "computeKernelMatrixColumn").
 //
-// Upper-triangular 128x128 tiles (bi <= bj). One CTA of 4 warps owns a column block bj
-// and T consecutive row tiles bi of it (T = 1 for shallow triangles, up to 4 for deep
-// ones, so the column prologue is paid once per T tiles):
+// Two forms, both evaluating every entry with term_pair()'s arithmetic and the control-point
+// summation order of fastron_score, so K_ij is bit-identical to fastron_score(alpha = e_i)
+// for M a power of two and the two forms give the same matrix bit for bit (tested); K is
+// exactly symmetric and K_ii = 1 exactly (d^2 = 0 gives 2^0 = rcp(1) = 1).
+//
+// Column-slot form (gram2_kernel, MP <= 8 — cfg3 and every M = 8 Gram): the scoring
+// kernel's structure with stores in place of the alpha-weighted sum — a CTA owns 384 columns
+// (3 per thread, in registers, read coalesced from the positions) and one 64-row tile
+// (TMA); see the comment above gram2_kernel. Mirror entries go out in whole 32-byte sectors.
+//
+// Tile form (gram_kernel, MP > 8 and layouts with ldk % 4 != 0): upper-triangular 128x128
+// tiles (bi <= bj). One CTA of 4 warps owns a column block bj and T consecutive row tiles bi
+// of it (T = 1 for shallow triangles, up to 4 for deep ones, so the column prologue is paid
+// once per T tiles):
 //  * COLUMN points live in registers: each lane holds CPL consecutive columns (2 at
 //    M <= 16, 1 above) as pre-scaled f32x2 control-point pairs (the packed records of
 //    the scoring kernel); a warp covers 32*CPL columns;
@@ -21,10 +32,8 @@
 //  * __launch_bounds__ asks for 4 resident CTAs at M <= 8 and 3 above.
 // JOINT = true builds the joint-space RBF Gram of the "Fastron RBF" baseline (PAPER.md:37,
 // :114-117) from zero-padded pseudo points: one RBF term of the whole squared distance.
-// The same term_pair() and control-point summation order as fastron_score make K_ij
-// bit-identical to fastron_score(alpha = e_i) for M a power of two; K is exactly
-// symmetric (each unordered pair is computed once, or as the exact mirror image on
-// diagonal tiles), and K_ii = 1 exactly (d^2 = 0 gives 2^0 = rcp(1) = 1).
+#include <cstdio>
+
 #include "fastron_device.cuh"
 #include "internal.h"
 
@@ -256,6 +265,304 @@ __global__ void __launch_bounds__(kGT, gram_min_blocks(MP))
   }
 }
 
+// ---------------------------------------------------------------------------------
+// K3, column-slot form: the scoring kernel's structure with a store in place of the
+// alpha-weighted accumulation.
+// ---------------------------------------------------------------------------------
+// A CTA of 128 threads owns a column block of W = 128 * QT columns (thread t holds columns
+// j0 + j * 128 + t, j < QT, as pre-scaled f32x2 pairs in registers, like a scoring thread's
+// QT queries) and ONE 64-row tile of the rows that block needs. Every row record is a
+// warp-broadcast LDS.128 + LDS.64 shared by the QT columns; per row a thread computes QT
+// entries with term_pair's arithmetic (accum_term, then pair_sum * 1/M: the same bits as
+// fastron_score(alpha = e_i) for M a power of two) and stores them: for a fixed row the
+// CTA's 128 threads write 128 consecutive floats (one 128-byte line per warp). The mirror
+// entries of 4 consecutive rows are kept in registers and written as one 16-byte segment
+// per column.
+// Which rows a block needs: with NBf = floor(n / W) full blocks and R = n - W NBf remainder
+// columns (E = ceil(R / 64) remainder row tiles), full block b takes the row tiles of
+// [0, W (b + 1)) — the tiles above its W x W diagonal block (entries stored twice, K[r][c]
+// and mirrored K[c][r]) and the diagonal block itself (computed in full, stored directly,
+// which covers it) — plus the E remainder tiles (stored twice). The remainder columns then
+// need only their own R x R diagonal block: E more units. (A remainder block treated like a
+// full one would cost a full block's column of tiles for R live columns: 84 of 630 units
+// at cfg3, R = 8.) Units: full block b has TPB (b + 1) + E of them (TPB = W / 64), so
+// units_before(b) = QT b (b + 1) + E b, inverted by a square root plus an exact step.
+// Predicated global stores with no compiler memory clobber: the kernel never reads K, so
+// letting the compiler move shared-memory loads across these stores is safe.
+__device__ __forceinline__ void st_global_if(float* p, float v, bool pred) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f32 [%0], %1;\n}" ::"l"(p), "f"(v),
+               "r"((int)pred));
+}
+__device__ __forceinline__ void st_global_v4_if(float* p, float a, float b, float c, float d, bool pred) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n @q st.global.v4.f32 [%0], {%1, %2, %3, %4};\n}" ::"l"(p),
+               "f"(a), "f"(b), "f"(c), "f"(d), "r"((int)pred));
+}
+
+constexpr int kG2NT = 128;
+__host__ __device__ constexpr int g2_qt(int mp) { return mp <= 16 ? 3 : 1; }
+
+// units before column block b (b <= NBf): QT b (b + 1) + E b
+__host__ __device__ inline int64_t g2_units_before(int64_t b, int qt, int64_t E) { return (int64_t)qt * b * (b + 1) + E * b; }
+
+struct G2Unit {
+  int64_t b;     // column block (NBf: the remainder block)
+  int64_t tile;  // row tile
+};
+
+__host__ __device__ inline G2Unit g2_unit(int64_t u, int64_t nbf, int qt, int64_t E) {
+  // largest b <= nbf with units_before(b) <= u: qt b^2 + (qt + E) b = u
+  const double A = (double)qt, B = (double)(qt + E);
+  int64_t b = (int64_t)((-B + sqrt(B * B + 4.0 * A * (double)u)) / (2.0 * A));
+  b = b < 0 ? 0 : b > nbf ? nbf : b;
+  while (b > 0 && g2_units_before(b, qt, E) > u) --b;
+  while (b < nbf && g2_units_before(b + 1, qt, E) <= u) ++b;
+  const int64_t k = u - g2_units_before(b, qt, E);
+  const int64_t tpb = 2 * qt, tf = nbf * tpb;  // first remainder tile
+  G2Unit r;
+  r.b = b;
+  r.tile = b == nbf ? tf + k : (k < tpb * (b + 1) ? k : tf + (k - tpb * (b + 1)));
+  return r;
+}
+
+// POW2: M is a power of two, so 1/M is an exact multiply (a compile-time choice: a runtime
+// branch per row would end the row's basic block and stop the compiler from overlapping
+// consecutive rows)
+// resident CTAs per SM the register allocation must allow (4 x 4 warps at M <= 8: the
+// scoring kernel's occupancy; 2 above)
+__host__ __device__ constexpr int g2_min_blocks(int mp) { return mp <= 8 ? 4 : 2; }
+
+template <int MP, int KIND, bool JOINT, bool POW2>
+__global__ void __launch_bounds__(kG2NT, g2_min_blocks(MP)) gram2_kernel(const float* __restrict__ packed,
+                                                                         const float4* __restrict__ pos, int64_t ldp,
+                                                                         float scale, int64_t n, int M, float inv_m,
+                                                                         float* __restrict__ K, int64_t ldk, int smask) {
+  constexpr int QT = g2_qt(MP);
+  constexpr int NP = MP / 2;
+  constexpr int W = kG2NT * QT;
+  constexpr int64_t TF = tile_floats(MP);
+  constexpr uint32_t TB = (uint32_t)tile_bytes(MP);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+  const float* T = reinterpret_cast<const float*>(smem_raw + 128);
+
+  const int64_t nbf = n / W, E = (n - nbf * W + kTileSupports - 1) / kTileSupports;
+  const G2Unit U = g2_unit(blockIdx.x, nbf, QT, E);
+  const int64_t j0 = U.b * W;
+  const int64_t r0 = U.tile * kTileSupports;
+  const int rows_here = (int)min((int64_t)kTileSupports, n - r0);
+  const bool mirror = r0 < j0 || r0 >= j0 + W;  // outside the block's diagonal square: store both
+  const int tid = threadIdx.x;
+#ifdef FASTRON_GRAM_PROF
+  unsigned long long t_start, t_pro = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+    mbar_expect_tx(bar, TB);
+    tma_bulk_g2s(smem_raw + 128, packed + U.tile * TF, TB, bar);
+  }
+
+  // the thread's QT columns straight from the control-point positions (SoA float4 [M][ldp]:
+  // consecutive threads read consecutive 16-byte elements, all QT * M loads in flight at
+  // once), scaled exactly as the pack kernel scales the row records (__fmul_rn by the same
+  // constant: the same bits); padded control points m >= M are 0 on the column side, so
+  // against a row's padded point the term is exactly 0. Reading the packed records instead
+  // (one 128-byte record per lane) put 32 lines behind every load instruction and left the
+  // columns arriving ~4 us after the CTA started (-DFASTRON_GRAM_PROF).
+  f2 ux[QT][NP], uy[QT][NP], uz[QT][NP];
+  bool col_ok[QT];
+#pragma unroll
+  for (int j = 0; j < QT; ++j) {
+    const int64_t c = j0 + j * kG2NT + tid;
+    col_ok[j] = c < n;
+    float px[MP], py[MP], pz[MP];
+#pragma unroll
+    for (int m = 0; m < MP; ++m) {
+      px[m] = py[m] = pz[m] = 0.0f;
+      if (m < M && col_ok[j]) {
+        const float4 v = __ldg(pos + (int64_t)m * ldp + c);
+        px[m] = __fmul_rn(v.x, scale);
+        py[m] = __fmul_rn(v.y, scale);
+        pz[m] = __fmul_rn(v.z, scale);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      ux[j][p] = pk(px[2 * p], px[2 * p + 1]);
+      uy[j][p] = pk(py[2 * p], py[2 * p + 1]);
+      uz[j][p] = pk(pz[2 * p], pz[2 * p + 1]);
+    }
+  }
+  float* Kd = K + r0 * ldk + j0 + tid;  // row r0, the thread's first column
+  float* const Kc = K + (j0 + tid) * ldk + r0;  // row c = j0 + tid, column r0: the mirror entries
+  const int64_t kc_step = (int64_t)kG2NT * ldk;  // to the thread's next column slot
+#ifdef FASTRON_GRAM_PROF
+  unsigned long long t_cols;
+  {
+    float sink = lo(ux[0][0]) + lo(uy[QT - 1][NP - 1]) + lo(uz[QT - 1][0]);
+    if (sink == -12345.f) K[0] = sink;  // the column loads have landed
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_cols));
+  }
+#endif
+  __syncthreads();  // the barrier's initialisation is visible before anyone waits on it
+  mbar_wait(bar, 0u);
+#ifdef FASTRON_GRAM_PROF
+  {
+    float sink = lo(ux[0][0]) + lo(uy[QT - 1][NP - 1]);
+    if (sink == -12345.f) K[0] = sink;  // the column loads have landed
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_pro));
+  }
+#endif
+
+  // 4 rows: their QT x 4 entries first (12 independent chains at QT = 3), then the direct
+  // stores (128 consecutive floats per row and column slot)
+  auto rows4 = [&](int c4, float (&v)[4][QT]) {
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const float* rec = T + (c4 + rr) * NP * 8;
+      f2 acc[QT];
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        const float4 xy = *reinterpret_cast<const float4*>(rec + p * 8);
+        const float2 zz = *reinterpret_cast<const float2*>(rec + p * 8 + 4);
+        const f2 vx = pk(xy.x, xy.y), vy = pk(xy.z, xy.w), vz = pk(zz.x, zz.y);
+        f2 dx[QT], dy[QT], dz[QT];
+#pragma unroll
+        for (int j = 0; j < QT; ++j) dx[j] = sub2(ux[j][p], vx);
+#pragma unroll
+        for (int j = 0; j < QT; ++j) dy[j] = sub2(uy[j][p], vy);
+#pragma unroll
+        for (int j = 0; j < QT; ++j) dz[j] = sub2(uz[j][p], vz);
+#pragma unroll
+        for (int j = 0; j < QT; ++j) {
+          if (JOINT) {  // squared joint-space distance, summed over all pseudo points
+            acc[j] = p == 0 ? mul2(dx[j], dx[j]) : fma2(dx[j], dx[j], acc[j]);
+            acc[j] = fma2(dy[j], dy[j], acc[j]);
+            acc[j] = fma2(dz[j], dz[j], acc[j]);
+          } else {
+            accum_term<KIND>(acc[j], dx[j], dy[j], dz[j], p == 0);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < QT; ++j) {
+        if (JOINT) {
+          const float d2 = pair_sum(acc[j]);
+          if (KIND == kGaussian) {
+            v[rr][j] = ex2_neg(d2);
+          } else {
+            const float w = 1.0f + d2;
+            v[rr][j] = rcp_approx(w * w);
+          }
+        } else {
+          const float ks = pair_sum(acc[j]);
+          v[rr][j] = POW2 ? ks * inv_m : __fdiv_rn(ks, (float)M);
+        }
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+#pragma unroll
+      for (int j = 0; j < QT; ++j)
+        st_global_if(Kd + j * kG2NT, v[rr][j], col_ok[j] && c4 + rr < rows_here && (smask & 1));
+      Kd += ldk;
+    }
+  };
+  // mirror entries K[c][r0 + c8 .. + 7] in whole 32-byte sectors (two 16-byte stores per
+  // column and 8 rows): 16-byte half-sector writes ran at ~1.2 TB/s against ~4 TB/s for
+  // full sectors (tools/store_probe.cu), which bounded the Gram at large N
+  auto mirror_rows = [&](int c, int nrows, const float (&v)[4][QT]) {  // rows c .. c + nrows - 1 (<= 4)
+#pragma unroll
+    for (int j = 0; j < QT; ++j) {
+      float* Kr = Kc + j * kc_step + c;
+      if (nrows == 4) {
+        st_global_v4_if(Kr, v[0][j], v[1][j], v[2][j], v[3][j], col_ok[j]);
+      } else {
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr) st_global_if(Kr + rr, v[rr][j], col_ok[j] && rr < nrows);
+      }
+    }
+  };
+  const bool do_mirror = mirror && (smask & 2);
+#pragma unroll 1
+  for (int c8 = 0; c8 < rows_here; c8 += 8) {
+    // both halves always (rows past n read the tile's zero padding and are never stored):
+    // one basic block, so the compiler may overlap the two halves
+    float va[4][QT], vb[4][QT];
+    rows4(c8, va);
+    rows4(c8 + 4, vb);
+    const bool second = c8 + 4 < rows_here;
+    if (do_mirror) {
+      if (c8 + 8 <= rows_here) {  // the usual case: one full sector per column
+#pragma unroll
+        for (int j = 0; j < QT; ++j) {
+          float* Kr = Kc + j * kc_step + c8;
+          st_global_v4_if(Kr, va[0][j], va[1][j], va[2][j], va[3][j], col_ok[j]);
+          st_global_v4_if(Kr + 4, vb[0][j], vb[1][j], vb[2][j], vb[3][j], col_ok[j]);
+        }
+      } else {  // the matrix's last rows
+        mirror_rows(c8, min(4, rows_here - c8), va);
+        if (second) mirror_rows(c8 + 4, rows_here - c8 - 4, vb);
+      }
+    }
+  }
+#ifdef FASTRON_GRAM_PROF
+  if (tid == 0) {
+    unsigned long long t_end;
+    unsigned int smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    printf("gram prof unit %d sm %u start %llu first-tile %llu end %llu rows %d cols %llu\n", blockIdx.x, smid, t_start,
+           t_pro - t_start, t_end, rows_here, t_cols - t_start);
+  }
+#endif
+}
+
+template <int MP, int KIND, bool JOINT, bool POW2>
+static cudaError_t run_gram2_m(const float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M,
+                               float* K, int64_t ldk, cudaStream_t st) {
+  constexpr int QT = g2_qt(MP);
+  constexpr int W = kG2NT * QT;
+  const int64_t nbf = n / W, R = n - nbf * W, E = (R + kTileSupports - 1) / kTileSupports;
+  const int64_t units = g2_units_before(nbf, QT, E) + (R > 0 ? E : 0);
+  if (units > 0x7fffffff) return cudaErrorInvalidValue;
+  const size_t smem = 128 + tile_bytes(MP) + (size_t)(kG2NT / 32) * 32 * MP * 16;  // barrier, row tile, column staging
+  static std::atomic<int> attr[kMaxDevices];
+  const int dev = device_slot();
+  if (!attr[dev].load()) {
+    cudaFuncSetAttribute(gram2_kernel<MP, KIND, JOINT, POW2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr[dev].store(1);
+  }
+  static const int smask = [] {  // probing only: 1 direct stores, 2 mirror stores
+    const char* e = getenv("FASTRON_GRAM_STORES");
+    return e ? atoi(e) : 3;
+  }();
+  gram2_kernel<MP, KIND, JOINT, POW2><<<(unsigned)units, kG2NT, smem, st>>>(packed, pos, ldp, scale, n, M,
+                                                                           1.0f / (float)M, K, ldk, smask);
+  g_launches.fetch_add(1);
+  return cudaGetLastError();
+}
+
+template <int MP, int KIND, bool JOINT>
+static cudaError_t run_gram(const float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M, float* K,
+                            int64_t ldk, cudaStream_t st);
+
+template <int MP, int KIND, bool JOINT>
+static cudaError_t run_gram2(const float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M,
+                             float* K, int64_t ldk, cudaStream_t st) {
+  // the mirror's 16-byte stores need ldk % 4 == 0 and a 16-byte aligned K; other layouts
+  // take the tile form
+  if ((ldk % 4) != 0 || (reinterpret_cast<uintptr_t>(K) & 15) != 0)
+    return run_gram<MP, KIND, JOINT>(packed, pos, ldp, scale, n, M, K, ldk, st);
+  // JOINT takes no 1/M; the exact-multiply instance exists where M can be a power of two
+  constexpr bool kCanPow2 = !JOINT && (MP & (MP - 1)) == 0;
+  if (JOINT) return run_gram2_m<MP, KIND, JOINT, true>(packed, pos, ldp, scale, n, M, K, ldk, st);
+  if (kCanPow2 && (M & (M - 1)) == 0)
+    return run_gram2_m<MP, KIND, JOINT, kCanPow2>(packed, pos, ldp, scale, n, M, K, ldk, st);
+  return run_gram2_m<MP, KIND, JOINT, false>(packed, pos, ldp, scale, n, M, K, ldk, st);
+}
+
 // row tiles per CTA: 1 while the triangle is only a few waves deep (occupancy first);
 // for deep triangles up to 4, keeping >= ~4 waves of units so the tail stays short
 // (measured at N = 20,000, M = 16: T = 1, 2, 4, 6, 8 -> 1.11, 1.03, 1.01, 1.03, 1.05 ms).
@@ -276,8 +583,9 @@ static int gram_rows_per_unit(int64_t tiles, int mp) {
   return (int)(T < 1 ? 1 : T > 4 ? 4 : T);
 }
 
-template <int MP, int KIND, bool JOINT = false>
-static cudaError_t run_gram(const float* packed, int64_t n, int M, float* K, int64_t ldk, cudaStream_t st) {
+template <int MP, int KIND, bool JOINT>
+static cudaError_t run_gram(const float* packed, const float4*, int64_t, float, int64_t n, int M, float* K, int64_t ldk,
+                            cudaStream_t st) {
   const int64_t nb = (n + kGB - 1) / kGB;
   const int64_t tiles = nb * (nb + 1) / 2;
   const int T = gram_rows_per_unit(tiles, MP);
@@ -297,31 +605,47 @@ static cudaError_t run_gram(const float* packed, int64_t n, int M, float* K, int
   return cudaGetLastError();
 }
 
-cudaError_t launch_gram_joint(const float* packed, int64_t n, int D, int kind, float* K, int64_t ldk, cudaStream_t st) {
+// Which form runs: the column-slot form up to MP = FASTRON_G2_MAXMP (A/B on one box, cfg3 and
+// N = 20,000 at M = 8: 56.5 vs 58.4 us, 0.59 vs 1.02 ms; M = 16 cfg5: the tile form 1.01 ms
+// against 1.18 — at 255 registers the column-slot form keeps 2 CTAs per SM, the tile form 3).
+#ifndef FASTRON_G2_MAXMP
+#define FASTRON_G2_MAXMP 8
+#endif
+template <int MP, int KIND, bool JOINT>
+static cudaError_t run_gram_any(const float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M,
+                                float* K, int64_t ldk, cudaStream_t st) {
+  if (MP <= FASTRON_G2_MAXMP) return run_gram2<MP, KIND, JOINT>(packed, pos, ldp, scale, n, M, K, ldk, st);
+  return run_gram<MP, KIND, JOINT>(packed, pos, ldp, scale, n, M, K, ldk, st);
+}
+#define FASTRON_RUN_GRAM run_gram_any
+
+cudaError_t launch_gram_joint(const float* packed, const float4* pts, float scale, int64_t n, int D, int kind, float* K,
+                              int64_t ldk, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int Mj = joint_points(D);
   switch (padded_m(Mj)) {
     case 2:
-      return kind == kGaussian ? run_gram<2, kGaussian, true>(packed, n, Mj, K, ldk, st)
-                               : run_gram<2, kRQ, true>(packed, n, Mj, K, ldk, st);
+      return kind == kGaussian ? FASTRON_RUN_GRAM<2, kGaussian, true>(packed, pts, n, scale, n, Mj, K, ldk, st)
+                               : FASTRON_RUN_GRAM<2, kRQ, true>(packed, pts, n, scale, n, Mj, K, ldk, st);
     case 4:
-      return kind == kGaussian ? run_gram<4, kGaussian, true>(packed, n, Mj, K, ldk, st)
-                               : run_gram<4, kRQ, true>(packed, n, Mj, K, ldk, st);
+      return kind == kGaussian ? FASTRON_RUN_GRAM<4, kGaussian, true>(packed, pts, n, scale, n, Mj, K, ldk, st)
+                               : FASTRON_RUN_GRAM<4, kRQ, true>(packed, pts, n, scale, n, Mj, K, ldk, st);
     case 6:
-      return kind == kGaussian ? run_gram<6, kGaussian, true>(packed, n, Mj, K, ldk, st)
-                               : run_gram<6, kRQ, true>(packed, n, Mj, K, ldk, st);
+      return kind == kGaussian ? FASTRON_RUN_GRAM<6, kGaussian, true>(packed, pts, n, scale, n, Mj, K, ldk, st)
+                               : FASTRON_RUN_GRAM<6, kRQ, true>(packed, pts, n, scale, n, Mj, K, ldk, st);
     default:
       return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t launch_gram(const float* packed, int64_t n, int M, int kind, float* K, int64_t ldk, cudaStream_t st) {
+cudaError_t launch_gram(const float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M, int kind,
+                        float* K, int64_t ldk, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int MP = padded_m(M);
 #define FASTRON_GCASE(mp)                                                                          \
   case mp:                                                                                         \
-    return kind == kGaussian ? run_gram<mp, kGaussian>(packed, n, M, K, ldk, st)                   \
-                             : run_gram<mp, kRQ>(packed, n, M, K, ldk, st);
+    return kind == kGaussian ? FASTRON_RUN_GRAM<mp, kGaussian, false>(packed, pos, ldp, scale, n, M, K, ldk, st) \
+                             : FASTRON_RUN_GRAM<mp, kRQ, false>(packed, pos, ldp, scale, n, M, K, ldk, st);
   switch (MP) {
     FASTRON_GCASE(2)
     FASTRON_GCASE(4)

@@ -200,48 +200,34 @@ def test_train_cluster_path_trace_exact():
     _assert_same_run(g, r)
 
 
-_GRAM_T_CHILD = r"""
-import sys, numpy as np, torch
-sys.path.insert(0, {root!r})
-import paper_1910_06451_b200 as fb, workloads as W
-out = []
-for M, n, kind in ((16, 1000, 0), (5, 777, 1), (8, 1, 0), (8, 129, 0)):
+@pytest.mark.parametrize("M,n,kind", [(16, 1000, 0), (5, 777, 1), (8, 1, 0), (8, 129, 0), (8, 385, 0), (4, 1153, 1),
+                                       (32, 300, 0)])
+def test_gram_forms_bit_identical(M, n, kind):
+    """K3 has two forms: the column-slot form (one 64-row tile per CTA, 16-byte mirror
+    stores; needs ldk % 4 == 0) and the tile form (any ldk). Both evaluate every entry with
+    the same term function and summation order, so an odd ldk (tile form) and a padded one
+    (column-slot form) must give the same matrix bit for bit — partial blocks, remainder
+    columns, ragged last tiles, odd M — and neither may write outside the n x n matrix."""
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
     rng = np.random.default_rng(M + n)
     base = W.arm7(8)
     robot = W.make_robot("t%d" % M, base.dh, rng.integers(0, 8, size=M), rng.uniform(-0.1, 0.1, size=(M, 3)))
     X = rng.uniform(-np.pi, np.pi, size=(n, 7)).astype(np.float32)
-    pos = fb.fastron_fk(robot, torch.from_numpy(X).cuda())
-    K = torch.full((n + 2, n + 8), -7.0, device="cuda")  # guard rows and columns
-    fb.fastron_gram(pos, kind, 5.0, K=K[:n, :n])
-    torch.cuda.synchronize()
-    out.append(K.cpu().numpy())
-np.savez({path!r}, *out)
-"""
-
-
-@pytest.mark.parametrize("T", [2, 3, 4])
-def test_gram_row_streaming_units_bit_identical(T, tmp_path):
-    """K3 streams T row tiles per CTA through a 2-stage TMA ring (T = 4 at the cfg5 size,
-    1 at small N). Forcing T (FASTRON_GRAM_T, read once per process) in a child process must
-    give the T = 1 matrix bit for bit — partial units, ragged last tiles, odd M, ldk > n."""
-    require_gpu()
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    code = _GRAM_T_CHILD.format(root=root, path=str(tmp_path / "k.npz"))
-    env = dict(os.environ, FASTRON_GRAM_T="1")
-    subprocess.run([sys.executable, "-c", code], check=True, env=env)
-    ref = np.load(tmp_path / "k.npz")
-    ref = [ref["arr_%d" % i] for i in range(len(ref.files))]
-    env["FASTRON_GRAM_T"] = str(T)
-    subprocess.run([sys.executable, "-c", code], check=True, env=env)
-    got = np.load(tmp_path / "k.npz")
-    for i, r in enumerate(ref):
-        g = got["arr_%d" % i]
-        n = r.shape[0] - 2
-        assert np.array_equal(g, r), (T, i)
+    pos = fb.fastron_fk(robot, dev(X))
+    out = []
+    for pad in (1, 8):  # ldk = n + 1 (odd: tile form), n + 8 (column-slot form when n % 4 == 0)
+        ld = n + pad + (0 if pad == 1 else (-(n + pad)) % 4)
+        K = torch.full((n + 2, ld), -7.0, device="cuda")  # guard rows and columns
+        fb.fastron_gram(pos, kind, 5.0, K=K[:n, :n])
+        torch.cuda.synchronize()
+        g = K.cpu().numpy()
         assert np.all(g[:, n:] == -7.0) and np.all(g[n:, :] == -7.0)
-        assert np.all(np.diag(g[:n, :n]) == 1.0) and np.array_equal(g[:n, :n], g[:n, :n].T)
+        g = g[:n, :n]
+        assert np.all(np.diag(g) == 1.0) and np.array_equal(g, g.T)
+        out.append(g)
+    assert np.array_equal(out[0], out[1])
 
 
 def test_train_every_cluster_size_same_run():

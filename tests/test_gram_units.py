@@ -1,40 +1,69 @@
-"""Host check of K3's work-unit enumeration (gram.cu units_before / unit_coords, restated
-here): for every T and block count the units cover each upper-triangle tile (bi <= bj)
-exactly once, which is what makes the streamed Gram write every entry of K."""
+"""Host check of K3's work-unit enumeration (gram.cu g2_units_before / g2_unit, restated
+here). Column blocks are W = 128 * QT wide; with NBf = n // W full blocks and R = n - W NBf
+remainder columns (E = ceil(R / 64) remainder row tiles), full block b takes the row tiles of
+[0, W (b + 1)) plus the E remainder tiles, and the remainder block takes its own E diagonal
+tiles; one unit = one (block, row tile). For every width and n the units must cover each
+such pair exactly once, and the direct + mirror stores they imply must write every entry of
+K exactly once (the diagonal square of a block: direct stores only)."""
 import math
 
 import pytest
 
 
-def units_before(b, T):
-    q, r = divmod(b, T)
-    return T * q * (q + 1) // 2 + r * (q + 1)
+def units_before(b, qt, E):
+    return qt * b * (b + 1) + E * b
 
 
-def unit_coords(u, nb, T):
-    b = int((math.sqrt(T * T + 8.0 * T * u) - T) * 0.5)
-    b = max(0, min(nb - 1, b))
-    while b > 0 and units_before(b, T) > u:
+def unit(u, nbf, qt, E):
+    A, B = float(qt), float(qt + E)
+    b = int((-B + math.sqrt(B * B + 4.0 * A * u)) / (2.0 * A))
+    b = max(0, min(nbf, b))
+    while b > 0 and units_before(b, qt, E) > u:
         b -= 1
-    while b + 1 < nb and units_before(b + 1, T) <= u:
+    while b < nbf and units_before(b + 1, qt, E) <= u:
         b += 1
-    return b, (u - units_before(b, T)) * T
+    k = u - units_before(b, qt, E)
+    tpb, tf = 2 * qt, nbf * 2 * qt
+    tile = tf + k if b == nbf else (k if k < tpb * (b + 1) else tf + (k - tpb * (b + 1)))
+    return b, tile
 
 
-@pytest.mark.parametrize("T", [1, 2, 3, 4, 7])
-@pytest.mark.parametrize("nb", [1, 2, 5, 40, 157, 1000])
-def test_units_cover_upper_triangle_once(T, nb):
-    tiles = []
-    for u in range(units_before(nb, T)):
-        bj, bi_first = unit_coords(u, nb, T)
-        assert 0 <= bi_first <= bj < nb
-        tiles += [(bi, bj) for bi in range(bi_first, min(bj, bi_first + T - 1) + 1)]
-    assert len(tiles) == nb * (nb + 1) // 2
-    assert set(tiles) == {(i, j) for j in range(nb) for i in range(j + 1)}
+def n_units(n, qt):
+    W = 128 * qt
+    nbf, R = n // W, n % W
+    E = -(-R // 64)
+    return units_before(nbf, qt, E) + (E if R else 0), nbf, E
 
 
-def test_units_sum_closed_form():
-    # units_before(b) = sum_{k=1..b} ceil(k / T)
-    for T in (1, 3, 4):
-        for b in range(60):
-            assert units_before(b, T) == sum(-(-k // T) for k in range(1, b + 1))
+@pytest.mark.parametrize("qt", [1, 3])
+@pytest.mark.parametrize("n", [1, 63, 64, 127, 383, 384, 385, 1000, 5000, 20000, 100_003])
+def test_units_cover_needed_row_tiles_once(qt, n):
+    W = 128 * qt
+    total, nbf, E = n_units(n, qt)
+    seen = {}
+    for u in range(total):
+        b, t = unit(u, nbf, qt, E)
+        seen[(b, t)] = seen.get((b, t), 0) + 1
+    tf = nbf * 2 * qt
+    want = {(b, t) for b in range(nbf) for t in range(2 * qt * (b + 1))}
+    want |= {(b, t) for b in range(nbf + (1 if n % W else 0)) for t in range(tf, tf + E)}
+    assert set(seen) == want and all(c == 1 for c in seen.values()), (n, qt)
+
+
+@pytest.mark.parametrize("qt,n", [(1, 300), (3, 1000), (3, 385), (1, 129), (3, 770)])
+def test_entries_written_once(qt, n):
+    W = 128 * qt
+    total, nbf, E = n_units(n, qt)
+    cnt = [[0] * n for _ in range(n)]
+    for u in range(total):
+        b, t = unit(u, nbf, qt, E)
+        j0 = b * W
+        cols = range(j0, min(n, j0 + W))
+        r0 = 64 * t
+        mirror = r0 < j0 or r0 >= j0 + W
+        for r in range(r0, min(n, r0 + 64)):
+            for c in cols:
+                cnt[r][c] += 1
+                if mirror:
+                    cnt[c][r] += 1
+    assert all(v == 1 for row in cnt for v in row), (qt, n)
