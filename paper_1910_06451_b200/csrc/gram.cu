@@ -299,7 +299,10 @@ __device__ __forceinline__ void st_global_v4_if(float* p, float a, float b, floa
 }
 
 constexpr int kG2NT = 128;
-__host__ __device__ constexpr int g2_qt(int mp) { return mp <= 16 ? 3 : 1; }
+#ifndef FASTRON_G2_QT16
+#define FASTRON_G2_QT16 2
+#endif
+__host__ __device__ constexpr int g2_qt(int mp) { return mp <= 8 ? 3 : mp <= 16 ? FASTRON_G2_QT16 : 1; }
 
 // units before column block b (b <= NBf): QT b (b + 1) + E b
 __host__ __device__ inline int64_t g2_units_before(int64_t b, int qt, int64_t E) { return (int64_t)qt * b * (b + 1) + E * b; }
@@ -329,7 +332,7 @@ __host__ __device__ inline G2Unit g2_unit(int64_t u, int64_t nbf, int qt, int64_
 // consecutive rows)
 // resident CTAs per SM the register allocation must allow (4 x 4 warps at M <= 8: the
 // scoring kernel's occupancy; 2 above)
-__host__ __device__ constexpr int g2_min_blocks(int mp) { return mp <= 8 ? 4 : 2; }
+__host__ __device__ constexpr int g2_min_blocks(int mp) { return mp <= 8 ? 4 : g2_qt(mp) <= 2 ? 3 : 2; }
 
 template <int MP, int KIND, bool JOINT, bool POW2>
 __global__ void __launch_bounds__(kG2NT, g2_min_blocks(MP)) gram2_kernel(const float* __restrict__ packed,
@@ -557,10 +560,13 @@ static cudaError_t run_gram2(const float* packed, const float4* pos, int64_t ldp
     return run_gram<MP, KIND, JOINT>(packed, pos, ldp, scale, n, M, K, ldk, st);
   // JOINT takes no 1/M; the exact-multiply instance exists where M can be a power of two
   constexpr bool kCanPow2 = !JOINT && (MP & (MP - 1)) == 0;
-  if (JOINT) return run_gram2_m<MP, KIND, JOINT, true>(packed, pos, ldp, scale, n, M, K, ldk, st);
-  if (kCanPow2 && (M & (M - 1)) == 0)
-    return run_gram2_m<MP, KIND, JOINT, kCanPow2>(packed, pos, ldp, scale, n, M, K, ldk, st);
-  return run_gram2_m<MP, KIND, JOINT, false>(packed, pos, ldp, scale, n, M, K, ldk, st);
+  if constexpr (JOINT) {
+    return run_gram2_m<MP, KIND, JOINT, true>(packed, pos, ldp, scale, n, M, K, ldk, st);
+  } else if constexpr (kCanPow2) {
+    if ((M & (M - 1)) == 0) return run_gram2_m<MP, KIND, JOINT, true>(packed, pos, ldp, scale, n, M, K, ldk, st);
+  }
+  if constexpr (!JOINT) return run_gram2_m<MP, KIND, JOINT, false>(packed, pos, ldp, scale, n, M, K, ldk, st);
+  return cudaErrorInvalidValue;
 }
 
 // row tiles per CTA: 1 while the triangle is only a few waves deep (occupancy first);
@@ -605,17 +611,18 @@ static cudaError_t run_gram(const float* packed, const float4*, int64_t, float, 
   return cudaGetLastError();
 }
 
-// Which form runs: the column-slot form up to MP = FASTRON_G2_MAXMP (A/B on one box, cfg3 and
-// N = 20,000 at M = 8: 56.5 vs 58.4 us, 0.59 vs 1.02 ms; M = 16 cfg5: the tile form 1.01 ms
-// against 1.18 — at 255 registers the column-slot form keeps 2 CTAs per SM, the tile form 3).
+// Which form runs: the column-slot form up to MP = FASTRON_G2_MAXMP, the tile form above and
+// for ldk % 4 != 0. A/B on one box (bit-identical matrices): cfg3 52.0 vs 58.4 us; N = 20,000
+// at M = 8 0.55 vs 1.02 ms; cfg5 (M = 16) with 2 columns per thread (168 registers, 3 CTAs
+// per SM) 0.896 vs 1.008 ms — with 3 (255 registers, 2 CTAs per SM) it was 1.05 ms.
 #ifndef FASTRON_G2_MAXMP
-#define FASTRON_G2_MAXMP 8
+#define FASTRON_G2_MAXMP 16
 #endif
 template <int MP, int KIND, bool JOINT>
 static cudaError_t run_gram_any(const float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M,
                                 float* K, int64_t ldk, cudaStream_t st) {
-  if (MP <= FASTRON_G2_MAXMP) return run_gram2<MP, KIND, JOINT>(packed, pos, ldp, scale, n, M, K, ldk, st);
-  return run_gram<MP, KIND, JOINT>(packed, pos, ldp, scale, n, M, K, ldk, st);
+  if constexpr (MP <= FASTRON_G2_MAXMP) return run_gram2<MP, KIND, JOINT>(packed, pos, ldp, scale, n, M, K, ldk, st);
+  else return run_gram<MP, KIND, JOINT>(packed, pos, ldp, scale, n, M, K, ldk, st);
 }
 #define FASTRON_RUN_GRAM run_gram_any
 

@@ -35,7 +35,7 @@ def n_units(n, qt):
     return units_before(nbf, qt, E) + (E if R else 0), nbf, E
 
 
-@pytest.mark.parametrize("qt", [1, 3])
+@pytest.mark.parametrize("qt", [1, 2, 3])
 @pytest.mark.parametrize("n", [1, 63, 64, 127, 383, 384, 385, 1000, 5000, 20000, 100_003])
 def test_units_cover_needed_row_tiles_once(qt, n):
     W = 128 * qt
@@ -50,7 +50,7 @@ def test_units_cover_needed_row_tiles_once(qt, n):
     assert set(seen) == want and all(c == 1 for c in seen.values()), (n, qt)
 
 
-@pytest.mark.parametrize("qt,n", [(1, 300), (3, 1000), (3, 385), (1, 129), (3, 770)])
+@pytest.mark.parametrize("qt,n", [(1, 300), (3, 1000), (3, 385), (1, 129), (3, 770), (2, 700), (2, 256)])
 def test_entries_written_once(qt, n):
     W = 128 * qt
     total, nbf, E = n_units(n, qt)
