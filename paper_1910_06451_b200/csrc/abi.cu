@@ -454,8 +454,6 @@ fastron_status fastron_gram(const float* pos, int64_t n, int64_t ldp, int32_t n_
   FASTRON_VALIDATE(vcheck_f32(pos, n_cp, 4 * n, 4 * ldp, stream, "pos"));
   float* packed = static_cast<float*>(workspace);
   const float c = kernel_scale(k);
-  cudaError_t e = launch_pack(reinterpret_cast<const float4*>(pos), ldp, nullptr, n, n_cp, c, packed, S(stream));
-  if (e != cudaSuccess) return cuda_status(e, "fastron_gram(pack)");
   return cuda_status(launch_gram(packed, reinterpret_cast<const float4*>(pos), ldp, c, n, n_cp, k.kind, K, ldk, S(stream)),
                      "fastron_gram");
 }
@@ -805,7 +803,6 @@ fastron_status fastron_gram_joint(const float* x, int64_t n, int64_t ldx, int32_
   cudaStream_t st = S(stream);
   const float c = kernel_scale(k);
   cudaError_t e = launch_joint_points(x, n, ldx, dof, pts, st);
-  if (e == cudaSuccess) e = launch_pack(pts, n, nullptr, n, Mj, c, packed, st, true);
   if (e == cudaSuccess) e = launch_gram_joint(packed, pts, c, n, dof, k.kind, K, ldk, st);
   return cuda_status(e, "fastron_gram_joint");
 }

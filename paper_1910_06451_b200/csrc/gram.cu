@@ -334,6 +334,12 @@ __host__ __device__ inline G2Unit g2_unit(int64_t u, int64_t nbf, int qt, int64_
 // scoring kernel's occupancy; 2 above)
 __host__ __device__ constexpr int g2_min_blocks(int mp) { return mp <= 8 ? 4 : g2_qt(mp) <= 2 ? 3 : 2; }
 
+// RP (rows packed): the row tile comes from the pack kernel's tiles by one TMA bulk copy (the
+// A/B winner above M = 8: cfg5 0.892 against 0.929 ms with rows from the positions); else
+// the CTA reads its rows from the positions itself and no pack kernel runs (cfg3 52.1 ->
+// 45.8 us per fastron_gram call: the pack launch and its round trip were ~6 us of it).
+__host__ __device__ constexpr bool g2_rows_packed(int mp) { return mp > 8; }
+
 template <int MP, int KIND, bool JOINT, bool POW2>
 __global__ void __launch_bounds__(kG2NT, g2_min_blocks(MP)) gram2_kernel(const float* __restrict__ packed,
                                                                          const float4* __restrict__ pos, int64_t ldp,
@@ -342,11 +348,15 @@ __global__ void __launch_bounds__(kG2NT, g2_min_blocks(MP)) gram2_kernel(const f
   constexpr int QT = g2_qt(MP);
   constexpr int NP = MP / 2;
   constexpr int W = kG2NT * QT;
+  constexpr int TS = kTileSupports;
+  constexpr bool RP = g2_rows_packed(MP);
   constexpr int64_t TF = tile_floats(MP);
-  constexpr uint32_t TB = (uint32_t)tile_bytes(MP);
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
-  const float* T = reinterpret_cast<const float*>(smem_raw + 128);
+  // planes (!RP): the tile's 64 row points s_xy[p][s] = (x_2p, x_2p+1, y_2p, y_2p+1) and
+  // s_z[p][s] = (z_2p, z_2p+1) of row s, pre-scaled (the packed record's contents)
+  __shared__ float4 s_xy[RP ? 1 : NP][TS];
+  __shared__ float2 s_z[RP ? 1 : NP][TS];
+  __shared__ __align__(128) float s_tile[RP ? TF : 4];  // RP: the packed tile (records, then alpha)
+  __shared__ uint64_t s_bar;
 
   const int64_t nbf = n / W, E = (n - nbf * W + kTileSupports - 1) / kTileSupports;
   const G2Unit U = g2_unit(blockIdx.x, nbf, QT, E);
@@ -359,11 +369,38 @@ __global__ void __launch_bounds__(kG2NT, g2_min_blocks(MP)) gram2_kernel(const f
   unsigned long long t_start, t_pro = 0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 #endif
-  if (tid == 0) {
-    mbar_init(bar, 1);
+  if (RP && tid == 0) {
+    mbar_init(&s_bar, 1);
     fence_barrier_init();
-    mbar_expect_tx(bar, TB);
-    tma_bulk_g2s(smem_raw + 128, packed + U.tile * TF, TB, bar);
+    mbar_expect_tx(&s_bar, (uint32_t)(TF * 4));
+    tma_bulk_g2s(s_tile, packed + U.tile * TF, (uint32_t)(TF * 4), &s_bar);
+  }
+  // !RP: the row points, straight from the positions: thread (s, p) loads control points 2p
+  // and 2p+1 of row r0 + s (consecutive threads, consecutive 16-byte elements) and scales
+  // them as the pack kernel scales a support (__fmul_rn by the same constant, the padded
+  // point m = M of an odd M at kPadCoord, rows past n zero) — the same bits as the packed
+  // tile, with no pack kernel and no copy in between
+  constexpr int RIT = (NP * TS + kG2NT - 1) / kG2NT;  // row items per thread (compile time: loads batched)
+  float4 ra[RIT], rb[RIT];
+#pragma unroll
+  for (int it = 0; it < RIT; ++it) {
+    const int idx = it * kG2NT + tid, sr = idx % TS, p = idx / TS;
+    const int64_t r = r0 + sr;
+    ra[it] = rb[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!RP && idx < NP * TS && r < n) {
+      ra[it] = __ldg(pos + (int64_t)(2 * p) * ldp + r);
+      if (2 * p + 1 < M) rb[it] = __ldg(pos + (int64_t)(2 * p + 1) * ldp + r);
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < RIT; ++it) {
+    const int idx = it * kG2NT + tid, sr = idx % TS, p = idx / TS;
+    if (RP || idx >= NP * TS) continue;
+    const float4 a = ra[it], b = rb[it];
+    float bx = __fmul_rn(b.x, scale), by = __fmul_rn(b.y, scale), bz = __fmul_rn(b.z, scale);
+    if (2 * p + 1 >= M) bx = by = bz = JOINT ? 0.0f : kPadCoord;
+    s_xy[p][sr] = make_float4(__fmul_rn(a.x, scale), bx, __fmul_rn(a.y, scale), by);
+    s_z[p][sr] = make_float2(__fmul_rn(a.z, scale), bz);
   }
 
   // the thread's QT columns straight from the control-point positions (SoA float4 [M][ldp]:
@@ -408,8 +445,8 @@ __global__ void __launch_bounds__(kG2NT, g2_min_blocks(MP)) gram2_kernel(const f
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_cols));
   }
 #endif
-  __syncthreads();  // the barrier's initialisation is visible before anyone waits on it
-  mbar_wait(bar, 0u);
+  __syncthreads();  // the row planes are complete (RP: the barrier's initialisation is visible)
+  if (RP) mbar_wait(&s_bar, 0u);
 #ifdef FASTRON_GRAM_PROF
   {
     float sink = lo(ux[0][0]) + lo(uy[QT - 1][NP - 1]);
@@ -423,12 +460,19 @@ __global__ void __launch_bounds__(kG2NT, g2_min_blocks(MP)) gram2_kernel(const f
   auto rows4 = [&](int c4, float (&v)[4][QT]) {
 #pragma unroll
     for (int rr = 0; rr < 4; ++rr) {
-      const float* rec = T + (c4 + rr) * NP * 8;
       f2 acc[QT];
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
-        const float4 xy = *reinterpret_cast<const float4*>(rec + p * 8);
-        const float2 zz = *reinterpret_cast<const float2*>(rec + p * 8 + 4);
+        float4 xy;
+        float2 zz;
+        if (RP) {
+          const float* rec = s_tile + (c4 + rr) * NP * 8 + p * 8;
+          xy = *reinterpret_cast<const float4*>(rec);
+          zz = *reinterpret_cast<const float2*>(rec + 4);
+        } else {
+          xy = s_xy[p][c4 + rr];
+          zz = s_z[p][c4 + rr];
+        }
         const f2 vx = pk(xy.x, xy.y), vy = pk(xy.z, xy.w), vz = pk(zz.x, zz.y);
         f2 dx[QT], dy[QT], dz[QT];
 #pragma unroll
@@ -523,36 +567,33 @@ __global__ void __launch_bounds__(kG2NT, g2_min_blocks(MP)) gram2_kernel(const f
 }
 
 template <int MP, int KIND, bool JOINT, bool POW2>
-static cudaError_t run_gram2_m(const float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M,
-                               float* K, int64_t ldk, cudaStream_t st) {
+static cudaError_t run_gram2_m(float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M, float* K,
+                               int64_t ldk, cudaStream_t st) {
+  if (g2_rows_packed(MP)) {
+    const cudaError_t pe = launch_pack(pos, ldp, nullptr, n, M, scale, packed, st, JOINT);
+    if (pe != cudaSuccess) return pe;
+  }
   constexpr int QT = g2_qt(MP);
   constexpr int W = kG2NT * QT;
   const int64_t nbf = n / W, R = n - nbf * W, E = (R + kTileSupports - 1) / kTileSupports;
   const int64_t units = g2_units_before(nbf, QT, E) + (R > 0 ? E : 0);
   if (units > 0x7fffffff) return cudaErrorInvalidValue;
-  const size_t smem = 128 + tile_bytes(MP) + (size_t)(kG2NT / 32) * 32 * MP * 16;  // barrier, row tile, column staging
-  static std::atomic<int> attr[kMaxDevices];
-  const int dev = device_slot();
-  if (!attr[dev].load()) {
-    cudaFuncSetAttribute(gram2_kernel<MP, KIND, JOINT, POW2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr[dev].store(1);
-  }
   static const int smask = [] {  // probing only: 1 direct stores, 2 mirror stores
     const char* e = getenv("FASTRON_GRAM_STORES");
     return e ? atoi(e) : 3;
   }();
-  gram2_kernel<MP, KIND, JOINT, POW2><<<(unsigned)units, kG2NT, smem, st>>>(packed, pos, ldp, scale, n, M,
-                                                                           1.0f / (float)M, K, ldk, smask);
+  gram2_kernel<MP, KIND, JOINT, POW2><<<(unsigned)units, kG2NT, 0, st>>>(packed, pos, ldp, scale, n, M,
+                                                                        1.0f / (float)M, K, ldk, smask);
   g_launches.fetch_add(1);
   return cudaGetLastError();
 }
 
 template <int MP, int KIND, bool JOINT>
-static cudaError_t run_gram(const float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M, float* K,
+static cudaError_t run_gram(float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M, float* K,
                             int64_t ldk, cudaStream_t st);
 
 template <int MP, int KIND, bool JOINT>
-static cudaError_t run_gram2(const float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M,
+static cudaError_t run_gram2(float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M,
                              float* K, int64_t ldk, cudaStream_t st) {
   // the mirror's 16-byte stores need ldk % 4 == 0 and a 16-byte aligned K; other layouts
   // take the tile form
@@ -590,8 +631,11 @@ static int gram_rows_per_unit(int64_t tiles, int mp) {
 }
 
 template <int MP, int KIND, bool JOINT>
-static cudaError_t run_gram(const float* packed, const float4*, int64_t, float, int64_t n, int M, float* K, int64_t ldk,
-                            cudaStream_t st) {
+static cudaError_t run_gram(float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M, float* K,
+                            int64_t ldk, cudaStream_t st) {
+  // the tile form streams packed support tiles: pack the points first
+  cudaError_t pe = launch_pack(pos, ldp, nullptr, n, M, scale, packed, st, JOINT);
+  if (pe != cudaSuccess) return pe;
   const int64_t nb = (n + kGB - 1) / kGB;
   const int64_t tiles = nb * (nb + 1) / 2;
   const int T = gram_rows_per_unit(tiles, MP);
@@ -619,14 +663,14 @@ static cudaError_t run_gram(const float* packed, const float4*, int64_t, float, 
 #define FASTRON_G2_MAXMP 16
 #endif
 template <int MP, int KIND, bool JOINT>
-static cudaError_t run_gram_any(const float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M,
+static cudaError_t run_gram_any(float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M,
                                 float* K, int64_t ldk, cudaStream_t st) {
   if constexpr (MP <= FASTRON_G2_MAXMP) return run_gram2<MP, KIND, JOINT>(packed, pos, ldp, scale, n, M, K, ldk, st);
   else return run_gram<MP, KIND, JOINT>(packed, pos, ldp, scale, n, M, K, ldk, st);
 }
 #define FASTRON_RUN_GRAM run_gram_any
 
-cudaError_t launch_gram_joint(const float* packed, const float4* pts, float scale, int64_t n, int D, int kind, float* K,
+cudaError_t launch_gram_joint(float* packed, const float4* pts, float scale, int64_t n, int D, int kind, float* K,
                               int64_t ldk, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int Mj = joint_points(D);
@@ -645,7 +689,7 @@ cudaError_t launch_gram_joint(const float* packed, const float4* pts, float scal
   }
 }
 
-cudaError_t launch_gram(const float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M, int kind,
+cudaError_t launch_gram(float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M, int kind,
                         float* K, int64_t ldk, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int MP = padded_m(M);

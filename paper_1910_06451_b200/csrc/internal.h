@@ -109,7 +109,7 @@ int joint_points(int D);
 cudaError_t launch_joint_points(const float* x, int64_t n, int64_t ldx, int D, float4* out, cudaStream_t st);
 cudaError_t launch_score_joint(const float4* qpts, int64_t nq, const float* packed, int64_t ns, int D, int kind,
                                float scale, float* score, int8_t* label, double* partial, cudaStream_t st);
-cudaError_t launch_gram_joint(const float* packed, const float4* pts, float scale, int64_t n, int D, int kind, float* K,
+cudaError_t launch_gram_joint(float* packed, const float4* pts, float scale, int64_t n, int D, int kind, float* K,
                               int64_t ldk, cudaStream_t st);
 
 // Model-update cycle pieces (update.cu)
@@ -136,8 +136,9 @@ cudaError_t count_nonfinite(const float* a, int64_t rows, int64_t cols, int64_t 
 cudaError_t count_nonfinite_f64(const double* a, int64_t n, cudaStream_t st, unsigned long long* out);
 cudaError_t count_bad_labels(const int8_t* y, int64_t n, cudaStream_t st, unsigned long long* out);
 
-// K3: Gram. packed: the pack kernel's tiles of pos (scaled by `scale`); pos: float4 [M][ldp]
-cudaError_t launch_gram(const float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M, int kind,
+// K3: Gram of the points pos (float4 [M][ldp]) with the kernel scale `scale`. packed: workspace
+// for packed support tiles (packed_bytes(n, M)), filled only when the tile form runs.
+cudaError_t launch_gram(float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M, int kind,
                         float* K, int64_t ldk, cudaStream_t st);
 
 // K5: Algorithm 1
