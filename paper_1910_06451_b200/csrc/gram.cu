@@ -293,6 +293,12 @@ __device__ __forceinline__ void st_global_if(float* p, float v, bool pred) {
   asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f32 [%0], %1;\n}" ::"l"(p), "f"(v),
                "r"((int)pred));
 }
+// one 32-byte store (st.global.v8.f32, sm_100): a whole sector per lane in one instruction
+__device__ __forceinline__ void st_global_v8_if(float* p, const float (&v)[8], bool pred) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %9, 0;\n @q st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n}" ::"l"(p),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "r"((int)pred));
+}
 __device__ __forceinline__ void st_global_v4_if(float* p, float a, float b, float c, float d, bool pred) {
   asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n @q st.global.v4.f32 [%0], {%1, %2, %3, %4};\n}" ::"l"(p),
                "f"(a), "f"(b), "f"(c), "f"(d), "r"((int)pred));
@@ -340,7 +346,9 @@ __host__ __device__ constexpr int g2_min_blocks(int mp) { return mp <= 8 ? 4 : g
 // 45.8 us per fastron_gram call: the pack launch and its round trip were ~6 us of it).
 __host__ __device__ constexpr bool g2_rows_packed(int mp) { return mp > 8; }
 
-template <int MP, int KIND, bool JOINT, bool POW2>
+// V8: the 8-row mirror sector as one 256-bit store per column (needs 32-byte aligned rows:
+// ldk % 8 == 0); a compile-time choice — as a runtime branch it cost cfg3 2 us (spills)
+template <int MP, int KIND, bool JOINT, bool POW2, bool V8>
 __global__ void __launch_bounds__(kG2NT, g2_min_blocks(MP)) gram2_kernel(const float* __restrict__ packed,
                                                                          const float4* __restrict__ pos, int64_t ldp,
                                                                          float scale, int64_t n, int M, float inv_m,
@@ -545,8 +553,13 @@ __global__ void __launch_bounds__(kG2NT, g2_min_blocks(MP)) gram2_kernel(const f
 #pragma unroll
         for (int j = 0; j < QT; ++j) {
           float* Kr = Kc + j * kc_step + c8;
-          st_global_v4_if(Kr, va[0][j], va[1][j], va[2][j], va[3][j], col_ok[j]);
-          st_global_v4_if(Kr + 4, vb[0][j], vb[1][j], vb[2][j], vb[3][j], col_ok[j]);
+          if (V8) {  // one 256-bit store per column (A/B: cfg3 45.8 -> 43.9 us, cfg5 0.90 -> 0.87 ms)
+            const float w8[8] = {va[0][j], va[1][j], va[2][j], va[3][j], vb[0][j], vb[1][j], vb[2][j], vb[3][j]};
+            st_global_v8_if(Kr, w8, col_ok[j]);
+          } else {
+            st_global_v4_if(Kr, va[0][j], va[1][j], va[2][j], va[3][j], col_ok[j]);
+            st_global_v4_if(Kr + 4, vb[0][j], vb[1][j], vb[2][j], vb[3][j], col_ok[j]);
+          }
         }
       } else {  // the matrix's last rows
         mirror_rows(c8, min(4, rows_here - c8), va);
@@ -582,8 +595,12 @@ static cudaError_t run_gram2_m(float* packed, const float4* pos, int64_t ldp, fl
     const char* e = getenv("FASTRON_GRAM_STORES");
     return e ? atoi(e) : 3;
   }();
-  gram2_kernel<MP, KIND, JOINT, POW2><<<(unsigned)units, kG2NT, 0, st>>>(packed, pos, ldp, scale, n, M,
-                                                                        1.0f / (float)M, K, ldk, smask);
+  if ((ldk % 8) == 0 && (reinterpret_cast<uintptr_t>(K) & 31) == 0)
+    gram2_kernel<MP, KIND, JOINT, POW2, true><<<(unsigned)units, kG2NT, 0, st>>>(packed, pos, ldp, scale, n, M,
+                                                                              1.0f / (float)M, K, ldk, smask);
+  else
+    gram2_kernel<MP, KIND, JOINT, POW2, false><<<(unsigned)units, kG2NT, 0, st>>>(packed, pos, ldp, scale, n, M,
+                                                                               1.0f / (float)M, K, ldk, smask);
   g_launches.fetch_add(1);
   return cudaGetLastError();
 }
