@@ -311,22 +311,23 @@ constexpr int kG2NT = 128;
 __host__ __device__ constexpr int g2_qt(int mp) { return mp <= 8 ? 3 : mp <= 16 ? FASTRON_G2_QT16 : 1; }
 
 // units before column block b (b <= NBf): QT b (b + 1) + E b
-__host__ __device__ inline int64_t g2_units_before(int64_t b, int qt, int64_t E) { return (int64_t)qt * b * (b + 1) + E * b; }
+// hb: half the unit rows per block width (W / UH / 2: QT for 64-row units, 2 QT for 32-row ones)
+__host__ __device__ inline int64_t g2_units_before(int64_t b, int hb, int64_t E) { return (int64_t)hb * b * (b + 1) + E * b; }
 
 struct G2Unit {
   int64_t b;     // column block (NBf: the remainder block)
   int64_t tile;  // row tile
 };
 
-__host__ __device__ inline G2Unit g2_unit(int64_t u, int64_t nbf, int qt, int64_t E) {
-  // largest b <= nbf with units_before(b) <= u: qt b^2 + (qt + E) b = u
-  const double A = (double)qt, B = (double)(qt + E);
+__host__ __device__ inline G2Unit g2_unit(int64_t u, int64_t nbf, int hb, int64_t E) {
+  // largest b <= nbf with units_before(b) <= u: hb b^2 + (hb + E) b = u
+  const double A = (double)hb, B = (double)(hb + E);
   int64_t b = (int64_t)((-B + sqrt(B * B + 4.0 * A * (double)u)) / (2.0 * A));
   b = b < 0 ? 0 : b > nbf ? nbf : b;
-  while (b > 0 && g2_units_before(b, qt, E) > u) --b;
-  while (b < nbf && g2_units_before(b + 1, qt, E) <= u) ++b;
-  const int64_t k = u - g2_units_before(b, qt, E);
-  const int64_t tpb = 2 * qt, tf = nbf * tpb;  // first remainder tile
+  while (b > 0 && g2_units_before(b, hb, E) > u) --b;
+  while (b < nbf && g2_units_before(b + 1, hb, E) <= u) ++b;
+  const int64_t k = u - g2_units_before(b, hb, E);
+  const int64_t tpb = 2 * hb, tf = nbf * tpb;  // unit tiles per block width; first remainder tile
   G2Unit r;
   r.b = b;
   r.tile = b == nbf ? tf + k : (k < tpb * (b + 1) ? k : tf + (k - tpb * (b + 1)));
@@ -348,7 +349,9 @@ __host__ __device__ constexpr bool g2_rows_packed(int mp) { return mp > 8; }
 
 // V8: the 8-row mirror sector as one 256-bit store per column (needs 32-byte aligned rows:
 // ldk % 8 == 0); a compile-time choice — as a runtime branch it cost cfg3 2 us (spills)
-template <int MP, int KIND, bool JOINT, bool POW2, bool V8>
+// UH: rows per unit (64, or 32 for shallow triangles: twice the units, so the block
+// scheduler can even out the SMs' loads); the packed row tiles (RP) need 64
+template <int MP, int KIND, bool JOINT, bool POW2, bool V8, int UH>
 __global__ void __launch_bounds__(kG2NT, g2_min_blocks(MP)) gram2_kernel(const float* __restrict__ packed,
                                                                          const float4* __restrict__ pos, int64_t ldp,
                                                                          float scale, int64_t n, int M, float inv_m,
@@ -356,8 +359,9 @@ __global__ void __launch_bounds__(kG2NT, g2_min_blocks(MP)) gram2_kernel(const f
   constexpr int QT = g2_qt(MP);
   constexpr int NP = MP / 2;
   constexpr int W = kG2NT * QT;
-  constexpr int TS = kTileSupports;
+  constexpr int TS = UH;
   constexpr bool RP = g2_rows_packed(MP);
+  static_assert(!RP || UH == kTileSupports, "packed row tiles are 64 rows");
   constexpr int64_t TF = tile_floats(MP);
   // planes (!RP): the tile's 64 row points s_xy[p][s] = (x_2p, x_2p+1, y_2p, y_2p+1) and
   // s_z[p][s] = (z_2p, z_2p+1) of row s, pre-scaled (the packed record's contents)
@@ -366,11 +370,12 @@ __global__ void __launch_bounds__(kG2NT, g2_min_blocks(MP)) gram2_kernel(const f
   __shared__ __align__(128) float s_tile[RP ? TF : 4];  // RP: the packed tile (records, then alpha)
   __shared__ uint64_t s_bar;
 
-  const int64_t nbf = n / W, E = (n - nbf * W + kTileSupports - 1) / kTileSupports;
-  const G2Unit U = g2_unit(blockIdx.x, nbf, QT, E);
+  constexpr int HB = W / UH / 2;
+  const int64_t nbf = n / W, E = (n - nbf * W + UH - 1) / UH;
+  const G2Unit U = g2_unit(blockIdx.x, nbf, HB, E);
   const int64_t j0 = U.b * W;
-  const int64_t r0 = U.tile * kTileSupports;
-  const int rows_here = (int)min((int64_t)kTileSupports, n - r0);
+  const int64_t r0 = U.tile * UH;
+  const int rows_here = (int)min((int64_t)UH, n - r0);
   const bool mirror = r0 < j0 || r0 >= j0 + W;  // outside the block's diagonal square: store both
   const int tid = threadIdx.x;
 #ifdef FASTRON_GRAM_PROF
@@ -579,6 +584,26 @@ __global__ void __launch_bounds__(kG2NT, g2_min_blocks(MP)) gram2_kernel(const f
 #endif
 }
 
+template <int MP, int KIND, bool JOINT, bool POW2, bool V8, int UH>
+static cudaError_t run_gram2_u(float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M, float* K,
+                               int64_t ldk, cudaStream_t st) {
+  constexpr int W = kG2NT * g2_qt(MP);
+  const int64_t nbf = n / W, R = n - nbf * W, E = (R + UH - 1) / UH;
+  const int64_t units = g2_units_before(nbf, W / UH / 2, E) + (R > 0 ? E : 0);
+  if (units > 0x7fffffff) return cudaErrorInvalidValue;
+  static const int smask = [] {  // probing only: 1 direct stores, 2 mirror stores
+    const char* e = getenv("FASTRON_GRAM_STORES");
+    return e ? atoi(e) : 3;
+  }();
+  gram2_kernel<MP, KIND, JOINT, POW2, V8, UH><<<(unsigned)units, kG2NT, 0, st>>>(packed, pos, ldp, scale, n, M,
+                                                                              1.0f / (float)M, K, ldk, smask);
+  g_launches.fetch_add(1);
+  return cudaGetLastError();
+}
+
+// 32-row units while the 64-row triangle fills at most half the resident slots (N = 2,560:
+// 27.6 -> 22.6 us); at cfg3 (560 units for 592 slots) they measured equal (44.6 vs 44.4 us:
+// the better balance over SMs is paid back in twice the CTA prologues); FASTRON_GRAM_UH overrides
 template <int MP, int KIND, bool JOINT, bool POW2>
 static cudaError_t run_gram2_m(float* packed, const float4* pos, int64_t ldp, float scale, int64_t n, int M, float* K,
                                int64_t ldk, cudaStream_t st) {
@@ -586,23 +611,23 @@ static cudaError_t run_gram2_m(float* packed, const float4* pos, int64_t ldp, fl
     const cudaError_t pe = launch_pack(pos, ldp, nullptr, n, M, scale, packed, st, JOINT);
     if (pe != cudaSuccess) return pe;
   }
-  constexpr int QT = g2_qt(MP);
-  constexpr int W = kG2NT * QT;
-  const int64_t nbf = n / W, R = n - nbf * W, E = (R + kTileSupports - 1) / kTileSupports;
-  const int64_t units = g2_units_before(nbf, QT, E) + (R > 0 ? E : 0);
-  if (units > 0x7fffffff) return cudaErrorInvalidValue;
-  static const int smask = [] {  // probing only: 1 direct stores, 2 mirror stores
-    const char* e = getenv("FASTRON_GRAM_STORES");
-    return e ? atoi(e) : 3;
-  }();
-  if ((ldk % 8) == 0 && (reinterpret_cast<uintptr_t>(K) & 31) == 0)
-    gram2_kernel<MP, KIND, JOINT, POW2, true><<<(unsigned)units, kG2NT, 0, st>>>(packed, pos, ldp, scale, n, M,
-                                                                              1.0f / (float)M, K, ldk, smask);
-  else
-    gram2_kernel<MP, KIND, JOINT, POW2, false><<<(unsigned)units, kG2NT, 0, st>>>(packed, pos, ldp, scale, n, M,
-                                                                               1.0f / (float)M, K, ldk, smask);
-  g_launches.fetch_add(1);
-  return cudaGetLastError();
+  const bool v8 = (ldk % 8) == 0 && (reinterpret_cast<uintptr_t>(K) & 31) == 0;
+  bool half = false;
+  if constexpr (!g2_rows_packed(MP)) {
+    constexpr int W = kG2NT * g2_qt(MP);
+    const int64_t nbf = n / W, E = (n - nbf * W + 63) / 64;
+    const int64_t units64 = g2_units_before(nbf, W / 64 / 2, E) + E;
+    static const int env = [] {
+      const char* e = getenv("FASTRON_GRAM_UH");
+      return e ? atoi(e) : 0;
+    }();
+    half = env ? env == 32 : 2 * units64 <= (int64_t)device_info().sms * g2_min_blocks(MP);
+    if (half)
+      return v8 ? run_gram2_u<MP, KIND, JOINT, POW2, true, 32>(packed, pos, ldp, scale, n, M, K, ldk, st)
+                : run_gram2_u<MP, KIND, JOINT, POW2, false, 32>(packed, pos, ldp, scale, n, M, K, ldk, st);
+  }
+  return v8 ? run_gram2_u<MP, KIND, JOINT, POW2, true, 64>(packed, pos, ldp, scale, n, M, K, ldk, st)
+            : run_gram2_u<MP, KIND, JOINT, POW2, false, 64>(packed, pos, ldp, scale, n, M, K, ldk, st);
 }
 
 template <int MP, int KIND, bool JOINT>
