@@ -210,6 +210,7 @@ def _time_rows(fb, torch, kind):
     """Secondary §8(a) rows, each timed on its own (not part of the headline step)."""
     rows = {}
     st = torch.cuda.current_stream()
+    R_MUFU = 148 * 16 * 1.965e9  # MUFU roofline, ops/s (DESIGN.md §6)
 
     def timed(fn, reps):
         fn()
@@ -222,9 +223,12 @@ def _time_rows(fb, torch, kind):
         e1.synchronize()
         return e0.elapsed_time(e1) / reps
 
-    def graphed(fn, reps):
+    def graphed(fn, reps, calls=1):
         """The same calls captured once into a CUDA graph and replayed (SURVEY §8(d):
-        separates launch overhead from kernel time)."""
+        separates launch overhead from kernel time). calls > 1 captures that many calls
+        back to back in one graph and returns the time per call: the device time of a call
+        in a stream of calls, with no host launch in between (one replay per `calls` calls;
+        a graph of one short call replayed from Python is bound by the host's launch rate)."""
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
@@ -233,8 +237,9 @@ def _time_rows(fb, torch, kind):
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            fn()
-        return timed(g.replay, reps)
+            for _ in range(calls):
+                fn()
+        return timed(g.replay, max(1, reps // calls)) / calls
 
     # cfg1: 3-DOF, 10k queries x 1k supports, M=4 (launch-latency scale)
     wl = W.score_workload("cfg1")
@@ -254,9 +259,12 @@ def _time_rows(fb, torch, kind):
 
     ms = timed(step1, 50)
     gms = graphed(step1, 50)
+    dms = graphed(step1, 200, calls=20)
     rows["cfg1_score"] = {"ms": ms, "checks_per_s": len(wl.queries) / ms * 1e3,
                           "kernel_evals_per_s": len(wl.queries) * len(wl.supports) / ms * 1e3,
-                          "graph_replay_ms": gms, "graph_checks_per_s": len(wl.queries) / gms * 1e3}
+                          "graph_replay_ms": gms, "graph_checks_per_s": len(wl.queries) / gms * 1e3,
+                          "graph_device_ms": dms, "graph_device_mufu_frac":
+                              len(wl.queries) * len(wl.supports) * wl.robot.n_cp / (dms * 1e-3) / R_MUFU}
     # cfg2: 1M x 2k, M=8
     wl = W.score_workload("cfg2")
     spos = fb.fastron_fk(wl.robot, torch.from_numpy(wl.supports).cuda())
@@ -283,10 +291,13 @@ def _time_rows(fb, torch, kind):
     gws = torch.empty(fb.load_library().fastron_gram_workspace_bytes(len(tw.X), 8), dtype=torch.uint8, device="cuda")
     ms = timed(lambda: fb.fastron_gram(pos, tw.kind, tw.gamma, K=K, workspace=gws), 10)
     gms = graphed(lambda: fb.fastron_gram(pos, tw.kind, tw.gamma, K=K, workspace=gws), 10)
+    dms = graphed(lambda: fb.fastron_gram(pos, tw.kind, tw.gamma, K=K, workspace=gws), 100, calls=10)
     n = len(tw.X)
+    pair_ops = n * (n + 1) // 2 * 8  # MUFU ops of the unique pairs (the algorithmic work)
     rows["cfg3_gram"] = {"ms": ms, "unique_pairs": n * (n + 1) // 2,
-                         "mufu_tops": n * n * 8 / 2 / ms * 1e-9, "write_GBps": n * n * 4 / ms * 1e-6,
-                         "graph_replay_ms": gms}
+                         "mufu_tops": pair_ops / ms * 1e-9, "mufu_frac_pairs": pair_ops / (ms * 1e-3) / R_MUFU,
+                         "write_GBps": n * n * 4 / ms * 1e-6, "graph_replay_ms": gms, "graph_device_ms": dms,
+                         "graph_device_mufu_frac_pairs": pair_ops / (dms * 1e-3) / R_MUFU}
     out = {}
 
     def train():
@@ -335,7 +346,7 @@ def _time_rows(fb, torch, kind):
     gws5 = torch.empty(fb.load_library().fastron_gram_workspace_bytes(n5, 16), dtype=torch.uint8, device="cuda")
     ms = timed(lambda: fb.fastron_gram(pos5, kind, 5.0, K=K5, workspace=gws5), 3)
     nb = (n5 + 127) // 128
-    rows["cfg5_gram"] = {"ms": ms, "n": n5, "mufu_frac": nb * (nb + 1) // 2 * 128 * 128 * 16 / (ms * 1e-3) / (148 * 16 * 1.965e9),
+    rows["cfg5_gram"] = {"ms": ms, "n": n5, "mufu_frac_pairs": n5 * (n5 + 1) // 2 * 16 / (ms * 1e-3) / R_MUFU,
                          "write_GBps": n5 * n5 * 4 / ms * 1e-6}
     # Algorithm 1 at cfg5 scale (N = 20,000, M = 16; labels by the moved cubes, R21): on the
     # 1.6 GB Gram and with lazily computed columns (no Gram; the point planes of the 16
@@ -426,7 +437,8 @@ def _time_rows(fb, torch, kind):
             wsl = torch.empty(max(256, fb.load_library().fastron_score_packed_workspace_bytes(nq, ns, 8)),
                               dtype=torch.uint8, device="cuda")
             fn = lambda: (fb.fastron_fk(hw.robot, qs, pos=qp), fb.fastron_score_packed(qp, mdl, sc, lb, workspace=wsl))
-            lat[f"S{ns}_q{nq}"] = {"stream_us": timed(fn, 200) * 1e3, "graph_us": graphed(fn, 200) * 1e3}
+            lat[f"S{ns}_q{nq}"] = {"stream_us": timed(fn, 200) * 1e3, "graph_us": graphed(fn, 200) * 1e3,
+                                   "graph_device_us": graphed(fn, 400, calls=20) * 1e3}
             if nq <= 32:  # fastron_query on device buffers: one fused launch for small batches
                 sp_ = sp.contiguous()
                 al_ = torch.from_numpy(hw.alpha[:ns]).cuda()
@@ -442,6 +454,7 @@ def _time_rows(fb, torch, kind):
             fqp = lambda: fb.fastron_query_packed(robot_c, qs, mdl, sc, lb, workspace=pws)
             lat[f"S{ns}_q{nq}"]["query_packed_stream_us"] = timed(fqp, 200) * 1e3
             lat[f"S{ns}_q{nq}"]["query_packed_graph_us"] = graphed(fqp, 200) * 1e3
+            lat[f"S{ns}_q{nq}"]["query_packed_device_us"] = graphed(fqp, 400, calls=20) * 1e3
     rows["small_batch_latency"] = lat
     # cfg4: 10k edges x 64 points, 3k supports, early exit
     ew = W.edge_workload()
