@@ -57,19 +57,19 @@ struct TrainResultDev {
   int32_t converged, n_support;
 };
 
-struct Cand {     // a (key, index) winner with its payload
-  uint64_t key;   // order-preserving bits of the value (-0 == +0)
-  double G;       // y F at the winner (min pass)
-  double Y;       // y alpha at the winner
+struct WCand {    // a warp winner: the key, its index and label (16 bytes, one STS.128)
+  uint64_t key;   // order-preserving bits of the value (-0 == +0); y F = key_value(key)
   int32_t idx;    // kNone if empty
   int32_t y;      // label at the winner
-  int32_t slot;   // lazy mode: column-cache slot of the winner's K column (-1: not cached)
-  int32_t pad;
 };
 
-struct __align__(16) CandBox {  // an inbox entry: 16-byte aligned for the vector DSMEM stores
-  Cand c;
-  int32_t pad2[2];
+struct __align__(16) Cand {  // a CTA winner with its payload (32 bytes: an inbox entry, two 16-byte DSMEM stores)
+  uint64_t key;
+  double Y;       // y alpha at the winner
+  int32_t idx;    // kNone if empty
+  int32_t y;
+  int32_t slot;   // lazy mode: column-cache slot of the winner's K column (-1: not cached)
+  int32_t pad;
 };
 
 struct Decision {
@@ -105,7 +105,8 @@ struct TrainArgs {
   float inv_m;
 };
 
-__device__ __forceinline__ Cand cand_none(bool for_max) { return Cand{for_max ? 0ull : ~0ull, 0.0, 0.0, kNone, 1, -1, 0}; }
+__device__ __forceinline__ Cand cand_none(bool for_max) { return Cand{for_max ? 0ull : ~0ull, 0.0, kNone, 1, -1, 0}; }
+__device__ __forceinline__ WCand wcand_none(bool for_max) { return WCand{for_max ? 0ull : ~0ull, kNone, 1}; }
 
 // Monotone map double -> uint64 (a < b  <=>  key(a) < key(b) for non-NaN; -0 == +0).
 __device__ __forceinline__ uint64_t order_key(double x) {
@@ -146,20 +147,6 @@ __device__ __forceinline__ int warp_argbest(uint64_t key, int idx, uint64_t& bke
   return own ? __ffs(own) - 1 : -1;
 }
 
-// Reduce a warp's worth of candidates (one per lane) to the lexicographic best, with its payload.
-template <bool MAX_KEY>
-__device__ __forceinline__ Cand warp_best(const Cand& c) {
-  Cand b;
-  const int bl = warp_argbest<MAX_KEY>(c.key, c.idx, b.key, b.idx);
-  const int src = bl < 0 ? 0 : bl;
-  b.G = __shfl_sync(0xffffffffu, c.G, src);
-  b.Y = __shfl_sync(0xffffffffu, c.Y, src);
-  b.y = __shfl_sync(0xffffffffu, c.y, src);
-  b.slot = __shfl_sync(0xffffffffu, c.slot, src);
-  b.pad = 0;
-  return b;
-}
-
 // The lane holding the warp's lexicographic best (key, idx) — warp_argbest without
 // distributing the winner (its owner already has it). -1: every lane empty.
 template <bool MAX_KEY>
@@ -183,7 +170,7 @@ __device__ __forceinline__ int warp_arglane(uint64_t key, int idx) {
 // CTA r's winner goes into slot [b][r] of every CTA's inbox by st.async (DSMEM stores that
 // complete transaction bytes on the receiver's mbarrier); each CTA then waits on its own
 // inbox barrier — a point-to-point hand-off instead of a cluster-wide barrier.
-constexpr uint32_t kCandMsgBytes = 40;  // key, G | Y, idx, y | slot, pad
+constexpr uint32_t kCandMsgBytes = 32;  // key, Y | idx, y, slot, pad
 
 __device__ __forceinline__ uint32_t cluster_addr(const void* p, int rank) {
   uint32_t r;
@@ -244,7 +231,7 @@ __device__ __forceinline__ Decision decide_min(const Cand& b, int64_t iters, int
   } else if (m <= 0.0 && (nnz < A.s_max || b.Y != 0.0)) {
     d.action = ACT_ADD;
     const double beta_i = b.y > 0 ? A.beta : 1.0;   // b_i = beta^(0.5 (y_i + 1))
-    const double sdelta = __dsub_rn(beta_i, b.G);   // y_i delta, delta = b_i y_i - F_i (Eq. 6)
+    const double sdelta = __dsub_rn(beta_i, m);     // y_i delta, delta = b_i y_i - F_i (Eq. 6); m = y_i F_i
     d.idx = b.idx;
     d.delta = b.y > 0 ? sdelta : -sdelta;
     d.newY = __dadd_rn(b.Y, sdelta);                 // y_i (alpha_i + delta) (Eq. 7)
@@ -277,7 +264,10 @@ __device__ __forceinline__ Decision decide_removal(Decision d, const Cand& b, in
 // GPTS: the lazy mode's point planes live in global memory (L2-resident scratch from the
 // workspace) instead of shared memory — slices too large for the 200 KB budget (N = 20,000
 // at M = 16: 1,250 points x 192 B per CTA). A computed column then reads its planes from L2.
-template <int EPT, int LMP, int LKIND, bool GPTS = false>
+// ONE: single-CTA instance (launched with C = 1 only) that keeps the winners' payload beside
+// the warp winners (the dependent shared-memory load after the REDUX costs it more than
+// the wider records: N = 1,000 0.80 against 0.81 us per iteration).
+template <int EPT, int LMP, int LKIND, bool GPTS = false, bool ONE = false>
 __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constant__ TrainArgs A) {
   constexpr bool LAZY = LMP > 0;
   constexpr int LNP = LAZY ? LMP / 2 : 1;
@@ -298,8 +288,10 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
                    : reinterpret_cast<f2*>(smem_raw + ((A.chunk * 8 + 15) & ~15ll));
   int32_t* s_slot = GPTS ? reinterpret_cast<int32_t*>(smem_raw + ((A.chunk * 8 + 15) & ~15ll))
                          : reinterpret_cast<int32_t*>(s_pts + (LAZY ? A.chunk * LNP * 3 : 0));
-  __shared__ Cand s_warp[2][kTrainWarps];
-  __shared__ CandBox s_inbox[2][kMaxCluster];               // C > 1: the CTA winners of an exchange
+  __shared__ __align__(16) WCand s_warp[2][kTrainWarps];
+  __shared__ double s_wY[2][ONE ? kTrainWarps : 1];      // ONE: Y and cache slot of the warp winners
+  __shared__ int32_t s_wslot[2][ONE ? kTrainWarps : 1];
+  __shared__ Cand s_inbox[2][kMaxCluster];                  // C > 1: the CTA winners of an exchange
   __shared__ __align__(8) uint64_t s_inbar[2];              // their arrival barriers
   __shared__ int32_t s_cta_cnt[2];
   __shared__ int32_t s_cnt[kTrainWarps];
@@ -376,6 +368,34 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
   // needs this CTA's message of the exchange in between, sent only after this CTA's
   // barrier that follows its reads.
   uint32_t ex = 0;
+  // The CTA's winner from the warp winners of buffer q (every lane of the calling warp gets
+  // it): a REDUX argbest over (key, idx), then the payload of the one winner. In a cluster
+  // (C > 1, warp 0 only) its label comes by a shuffle and Y (and the lazy mode's cache
+  // slot) by a broadcast load from this CTA's shared memory, so the warp stage moves 16
+  // bytes per warp and never touches Y (cfg3, C = 5: 1.155 -> 1.128 us per iteration).
+  auto cta_best = [&](int q, bool for_max) -> Cand {
+    const WCand w = lane < kTrainWarps ? s_warp[q][lane] : wcand_none(for_max);
+    Cand b = cand_none(for_max);
+    if (ONE) {
+      // one CTA: the owner lanes stored Y (and the slot) beside their warp winners, every
+      // lane holds its warp's payload before the REDUX and the winner's comes by shuffles
+      const double Yl = lane < kTrainWarps ? s_wY[q][lane] : 0.0;
+      const int sl = (LAZY && lane < kTrainWarps) ? s_wslot[q][lane] : -1;
+      const int wl = for_max ? warp_argbest<true>(w.key, w.idx, b.key, b.idx) : warp_argbest<false>(w.key, w.idx, b.key, b.idx);
+      const int src = wl < 0 ? 0 : wl;
+      b.y = __shfl_sync(0xffffffffu, w.y, src);
+      b.Y = __shfl_sync(0xffffffffu, Yl, src);
+      if (LAZY) b.slot = __shfl_sync(0xffffffffu, sl, src);
+      return b;
+    }
+    const int wl = for_max ? warp_argbest<true>(w.key, w.idx, b.key, b.idx) : warp_argbest<false>(w.key, w.idx, b.key, b.idx);
+    b.y = __shfl_sync(0xffffffffu, w.y, wl < 0 ? 0 : wl);
+    if (wl >= 0) {
+      b.Y = s_Y[b.idx - lo];
+      if (LAZY) b.slot = s_slot[b.idx - lo];
+    }
+    return b;
+  };
   auto cluster_best = [&](const Cand& mine, bool for_max) -> Cand {  // mine: warp 0's CTA winner
     const int b = (int)(ex & 1u);
     if (warp == 0) {
@@ -383,17 +403,28 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
       if (lane < C) {  // lane r delivers this CTA's winner to rank r
         const uint32_t dst = cluster_addr(&s_inbox[b][rank], lane);
         const uint32_t bar = cluster_addr(&s_inbar[b], lane);
-        st_async_v2b64(dst, mine.key, (uint64_t)__double_as_longlong(mine.G), bar);
-        st_async_v2b64(dst + 16, (uint64_t)__double_as_longlong(mine.Y),
-                       ((uint64_t)(uint32_t)mine.y << 32) | (uint32_t)mine.idx, bar);
-        st_async_v2b32(dst + 32, (uint32_t)mine.slot, 0u, bar);
+        st_async_v2b64(dst, mine.key, (uint64_t)__double_as_longlong(mine.Y), bar);
+        st_async_v2b64(dst + 16, ((uint64_t)(uint32_t)mine.y << 32) | (uint32_t)mine.idx,
+                       (uint64_t)(uint32_t)mine.slot, bar);
       }
     }
     mbar_wait_cluster(&s_inbar[b], (ex >> 1) & 1u);
     ++ex;
-
-    return for_max ? warp_best<true>(lane < C ? s_inbox[b][lane].c : cand_none(true))
-                   : warp_best<false>(lane < C ? s_inbox[b][lane].c : cand_none(false));
+    // the C CTA winners: argbest over (key, idx), the winner's payload by a broadcast load
+    uint64_t key = for_max ? 0ull : ~0ull;
+    int idx = kNone;
+    if (lane < C) {
+      key = s_inbox[b][lane].key;
+      idx = s_inbox[b][lane].idx;
+    }
+    Cand best = cand_none(for_max);
+    const int wl = for_max ? warp_argbest<true>(key, idx, best.key, best.idx) : warp_argbest<false>(key, idx, best.key, best.idx);
+    if (wl >= 0) {
+      best.Y = s_inbox[b][wl].Y;
+      best.y = s_inbox[b][wl].y;
+      best.slot = s_inbox[b][wl].slot;
+    }
+    return best;
   };
 
   int64_t iters = 0, n_add = 0, n_remove = 0;
@@ -504,11 +535,15 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
       PROF_MARK(6);
       const int wl = warp_arglane<false>(okey, my_idx);
       PROF_MARK(7);
-      if (lane == wl) {  // the owner lane writes the warp winner with its payload
-        const int jw = mkk * kTrainNT + tid;
-        s_warp[parity][warp] = Cand{okey, mk, s_Y[jw], my_idx, ((yneg >> mkk) & 1u) ? -1 : 1, LAZY ? s_slot[jw] : -1, 0};
+      if (lane == wl) {  // the owner lane writes the warp winner
+        s_warp[parity][warp] = WCand{okey, my_idx, ((yneg >> mkk) & 1u) ? -1 : 1};
+        if (ONE) {
+          const int jw = mkk * kTrainNT + tid;
+          s_wY[parity][warp] = s_Y[jw];
+          if (LAZY) s_wslot[parity][warp] = s_slot[jw];
+        }
       } else if (wl < 0 && lane == 0) {
-        s_warp[parity][warp] = cand_none(false);
+        s_warp[parity][warp] = wcand_none(false);
       }
     }
     PROF_MARK(1);
@@ -520,11 +555,10 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
     //         the candidate buffers are double-buffered by parity) ----
     Decision d;
     if (C == 1) {
-      const Cand best = warp_best<false>(lane < kTrainWarps ? s_warp[parity][lane] : cand_none(false));
-      d = decide_min(best, iters, nnz, nfree, A);
+      d = decide_min(cta_best(parity, false), iters, nnz, nfree, A);
     } else {
       Cand mine = cand_none(false);
-      if (warp == 0) mine = warp_best<false>(lane < kTrainWarps ? s_warp[parity][lane] : cand_none(false));
+      if (warp == 0) mine = cta_best(parity, false);
       const Cand best = cluster_best(mine, false);
       d = decide_min(best, iters, nnz, nfree, A);
     }
@@ -550,19 +584,22 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
         const uint64_t rkey = order_key(rk);
         const int wl = warp_arglane<true>(rkey, ridx);
         if (lane == wl) {
-          const int jw = rkk * kTrainNT + tid;
-          s_warp[q][warp] = Cand{rkey, 0.0, s_Y[jw], ridx, ((yneg >> rkk) & 1u) ? -1 : 1, LAZY ? s_slot[jw] : -1, 0};
+          s_warp[q][warp] = WCand{rkey, ridx, ((yneg >> rkk) & 1u) ? -1 : 1};
+          if (ONE) {
+            const int jw = rkk * kTrainNT + tid;
+            s_wY[q][warp] = s_Y[jw];
+            if (LAZY) s_wslot[q][warp] = s_slot[jw];
+          }
         } else if (wl < 0 && lane == 0) {
-          s_warp[q][warp] = cand_none(true);
+          s_warp[q][warp] = wcand_none(true);
         }
       }
       __syncthreads();
       if (C == 1) {
-        const Cand best = warp_best<true>(lane < kTrainWarps ? s_warp[q][lane] : cand_none(true));
-        d = decide_removal(d, best, nfree, A);
+        d = decide_removal(d, cta_best(q, true), nfree, A);
       } else {
         Cand mine = cand_none(true);
-        if (warp == 0) mine = warp_best<true>(lane < kTrainWarps ? s_warp[q][lane] : cand_none(true));
+        if (warp == 0) mine = cta_best(q, true);
         const Cand best = cluster_best(mine, true);
         d = decide_removal(d, best, nfree, A);
       }
@@ -687,13 +724,14 @@ static int train_cluster_size(int64_t n, int64_t chunk_max) {
   return (int)C;
 }
 
-template <int EPT, int LMP = 0, int LKIND = 0, bool GPTS = false>
+template <int EPT, int LMP = 0, int LKIND = 0, bool GPTS = false, bool ONE = false>
 static cudaError_t launch_ept(const TrainArgs& A, int C, cudaStream_t st, size_t smem) {
   static std::atomic<int> attr[kMaxDevices];
   const int dev = device_slot();
   if (!attr[dev].load()) {
-    cudaFuncSetAttribute(train_kernel<EPT, LMP, LKIND, GPTS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(train_kernel<EPT, LMP, LKIND, GPTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(train_kernel<EPT, LMP, LKIND, GPTS, ONE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(train_kernel<EPT, LMP, LKIND, GPTS, ONE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         220 * 1024);
     attr[dev].store(1);
   }
   cudaLaunchConfig_t cfg = {};
@@ -708,7 +746,7 @@ static cudaError_t launch_ept(const TrainArgs& A, int C, cudaStream_t st, size_t
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, train_kernel<EPT, LMP, LKIND, GPTS>, A);
+  return cudaLaunchKernelEx(&cfg, train_kernel<EPT, LMP, LKIND, GPTS, ONE>, A);
 }
 
 cudaError_t launch_train(const float* K, int64_t n, int64_t ldk, const int8_t* y, double beta, int64_t iter_max,
@@ -744,7 +782,9 @@ cudaError_t launch_train(const float* K, int64_t n, int64_t ldk, const int8_t* y
   // the smallest instance that covers the slice: dead slots still cost a load and an update
   // instances at sixths of the register budget (4, 8, ..., 24 slots at 256 threads)
   constexpr int E = kMaxEPT / 6;
-  if (ept <= E) e = launch_ept<E>(A, C, st, smem);
+  if (C == 1 && ept <= E) e = launch_ept<E, 0, 0, false, true>(A, C, st, smem);
+  else if (C == 1 && ept <= 2 * E) e = launch_ept<2 * E, 0, 0, false, true>(A, C, st, smem);
+  else if (ept <= E) e = launch_ept<E>(A, C, st, smem);
   else if (ept <= 2 * E) e = launch_ept<2 * E>(A, C, st, smem);
   else if (ept <= 3 * E) e = launch_ept<3 * E>(A, C, st, smem);
   else if (ept <= 4 * E) e = launch_ept<4 * E>(A, C, st, smem);
