@@ -166,6 +166,38 @@ __device__ __forceinline__ int warp_arglane(uint64_t key, int idx) {
   return own ? __ffs(own) - 1 : -1;
 }
 
+// (key, idx) of a beats that of b: smaller key (MAX_KEY: larger), then smaller idx. Empty
+// entries carry the neutral key and idx = kNone (the largest index), so they lose to any
+// live entry — the order warp_argbest implements, as a plain comparison.
+template <bool MAX_KEY>
+__device__ __forceinline__ bool cand_beats(uint64_t ka, int ia, uint64_t kb, int ib) {
+  // bitwise, not short-circuit: the compiler otherwise branches at every comparison
+  return (bool)((int)(MAX_KEY ? ka > kb : ka < kb) | ((int)(ka == kb) & (int)((unsigned)ia < (unsigned)ib)));
+}
+
+// The best of up to 8 candidates every lane has read itself (broadcast loads): a 3-level
+// selection tree in registers. Against warp_argbest (REDUX -> vote -> shuffles, each a
+// dependent MIO round trip, ~130 cycles + payload) this is 8 independent loads and 3
+// dependent compare-select levels, but ~100 instructions: it pays where one warp runs it
+// (the CTA stage of a cluster: N = 8,446, C = 9 1.139 -> 1.128 us per iteration), not
+// where all warps run it redundantly.
+template <bool MAX_KEY>
+__device__ __forceinline__ Cand best_of8(Cand (&e)[8]) {
+#pragma unroll
+  for (int st = 4; st >= 1; st >>= 1)
+#pragma unroll
+    for (int i = 0; i < st; ++i)
+    {  // field-wise selects (no branches)
+      const bool t = cand_beats<MAX_KEY>(e[i + st].key, e[i + st].idx, e[i].key, e[i].idx);
+      e[i].key = t ? e[i + st].key : e[i].key;
+      e[i].Y = t ? e[i + st].Y : e[i].Y;
+      e[i].idx = t ? e[i + st].idx : e[i].idx;
+      e[i].y = t ? e[i + st].y : e[i].y;
+      e[i].slot = t ? e[i + st].slot : e[i].slot;
+    }
+  return e[0];
+}
+
 // ---- cluster exchange of the CTA winners (C > 1) ----
 // CTA r's winner goes into slot [b][r] of every CTA's inbox by st.async (DSMEM stores that
 // complete transaction bytes on the receiver's mbarrier); each CTA then waits on its own
@@ -368,19 +400,34 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
   // needs this CTA's message of the exchange in between, sent only after this CTA's
   // barrier that follows its reads.
   uint32_t ex = 0;
+#ifdef FASTRON_TRAIN_PROF
+  unsigned long long prof[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long prof_miss = 0, n_miss = 0;  // lazy mode: cycles in computed columns
+  unsigned long long tp = clock64();
+#define PROF_MARK(i)                         \
+  do {                                       \
+    const unsigned long long tn = clock64(); \
+    prof[i] += tn - tp;                      \
+    tp = tn;                                 \
+  } while (0)
+#else
+#define PROF_MARK(i) \
+  do {               \
+  } while (0)
+#endif
   // The CTA's winner from the warp winners of buffer q (every lane of the calling warp gets
-  // it): a REDUX argbest over (key, idx), then the payload of the one winner. In a cluster
-  // (C > 1, warp 0 only) its label comes by a shuffle and Y (and the lazy mode's cache
-  // slot) by a broadcast load from this CTA's shared memory, so the warp stage moves 16
-  // bytes per warp and never touches Y (cfg3, C = 5: 1.155 -> 1.128 us per iteration).
+  // it): a selection tree over the 8 records, then the payload of the one winner: in a cluster
+  // (C > 1, warp 0 only) Y (and the lazy mode's cache slot) by a broadcast load from this
+  // CTA's shared memory, so the warp stage moves 16 bytes per warp and never touches Y
+  // (cfg3, C = 5: 1.155 -> 1.128 us per iteration).
   auto cta_best = [&](int q, bool for_max) -> Cand {
-    const WCand w = lane < kTrainWarps ? s_warp[q][lane] : wcand_none(for_max);
-    Cand b = cand_none(for_max);
     if (ONE) {
-      // one CTA: the owner lanes stored Y (and the slot) beside their warp winners, every
-      // lane holds its warp's payload before the REDUX and the winner's comes by shuffles
+      // one CTA, every warp redundantly: REDUX argbest, the payload the owner lanes stored
+      // beside their warp winners by shuffles
+      const WCand w = lane < kTrainWarps ? s_warp[q][lane] : wcand_none(for_max);
       const double Yl = lane < kTrainWarps ? s_wY[q][lane] : 0.0;
       const int sl = (LAZY && lane < kTrainWarps) ? s_wslot[q][lane] : -1;
+      Cand b = cand_none(for_max);
       const int wl = for_max ? warp_argbest<true>(w.key, w.idx, b.key, b.idx) : warp_argbest<false>(w.key, w.idx, b.key, b.idx);
       const int src = wl < 0 ? 0 : wl;
       b.y = __shfl_sync(0xffffffffu, w.y, src);
@@ -388,9 +435,34 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
       if (LAZY) b.slot = __shfl_sync(0xffffffffu, sl, src);
       return b;
     }
-    const int wl = for_max ? warp_argbest<true>(w.key, w.idx, b.key, b.idx) : warp_argbest<false>(w.key, w.idx, b.key, b.idx);
-    b.y = __shfl_sync(0xffffffffu, w.y, wl < 0 ? 0 : wl);
-    if (wl >= 0) {
+    if (C == 1) {
+      // one CTA without the ONE instance (lazy mode, forced C): REDUX argbest, the winner's
+      // payload by a broadcast load
+      const WCand w = lane < kTrainWarps ? s_warp[q][lane] : wcand_none(for_max);
+      Cand b = cand_none(for_max);
+      const int wl = for_max ? warp_argbest<true>(w.key, w.idx, b.key, b.idx) : warp_argbest<false>(w.key, w.idx, b.key, b.idx);
+      b.y = __shfl_sync(0xffffffffu, w.y, wl < 0 ? 0 : wl);
+      if (wl >= 0) {
+        b.Y = s_Y[b.idx - lo];
+        if (LAZY) b.slot = s_slot[b.idx - lo];
+      }
+      return b;
+    }
+    // cluster (warp 0 only): every lane reads the 8 records itself and selects in registers
+    static_assert(kTrainWarps <= 8, "best_of8 covers the warp winners of one CTA");
+    Cand e[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      e[w] = cand_none(for_max);
+      if (w < kTrainWarps) {
+        const WCand c = s_warp[q][w];
+        e[w].key = c.key;
+        e[w].idx = c.idx;
+        e[w].y = c.y;
+      }
+    }
+    Cand b = for_max ? best_of8<true>(e) : best_of8<false>(e);
+    if (b.idx != kNone) {
       b.Y = s_Y[b.idx - lo];
       if (LAZY) b.slot = s_slot[b.idx - lo];
     }
@@ -408,9 +480,14 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
                        (uint64_t)(uint32_t)mine.slot, bar);
       }
     }
+    PROF_MARK(8);
     mbar_wait_cluster(&s_inbar[b], (ex >> 1) & 1u);
+    PROF_MARK(9);
     ++ex;
-    // the C CTA winners: argbest over (key, idx), the winner's payload by a broadcast load
+    // the C CTA winners: REDUX argbest over (key, idx), the winner's payload by a broadcast
+    // load. (A selection tree over entries every lane reads itself was measured slower here,
+    // 295 -> 588 cycles: all 8 warps run this stage redundantly, so its ~140 instructions
+    // per warp are issue-bound, while the REDUX path is ~20.)
     uint64_t key = for_max ? 0ull : ~0ull;
     int idx = kNone;
     if (lane < C) {
@@ -424,6 +501,7 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
       best.y = s_inbox[b][wl].y;
       best.slot = s_inbox[b][wl].slot;
     }
+    PROF_MARK(10);
     return best;
   };
 
@@ -435,21 +513,6 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
   int parity = 0;
   int converged = 0;
 
-#ifdef FASTRON_TRAIN_PROF
-  unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  unsigned long long prof_miss = 0, n_miss = 0;  // lazy mode: cycles in computed columns
-  unsigned long long tp = clock64();
-#define PROF_MARK(i)                         \
-  do {                                       \
-    const unsigned long long tn = clock64(); \
-    prof[i] += tn - tp;                      \
-    tp = tn;                                 \
-  } while (0)
-#else
-#define PROF_MARK(i) \
-  do {               \
-  } while (0)
-#endif
   for (;;) {
     // ---- 1. all loads of the pending K row, then the fused update + min scan ----
     float kr[EPT];
@@ -635,10 +698,10 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
 #ifdef FASTRON_TRAIN_PROF
   if (tid == 0 && rank == 0 && n_miss) printf("train prof computed columns %llu, %.0f cycles each\n", n_miss, (double)prof_miss / n_miss);
   if (tid == 0 && rank == 0)
-    printf("train prof cycles/iter: scan %.0f merge+key %.0f argbest %.0f payload %.0f bar %.0f decide %.0f - %.0f tail %.0f (iters %lld)\n",
+    printf("train prof cycles/iter: scan %.0f merge+key %.0f argbest %.0f payload %.0f bar %.0f | cta-best+send %.0f inbox-wait %.0f inbox-best %.0f decide %.0f - %.0f tail %.0f (iters %lld)\n",
            (double)prof[0] / iters, (double)prof[6] / iters, (double)prof[7] / iters, (double)prof[1] / iters,
-           (double)prof[2] / iters, (double)prof[3] / iters, (double)prof[4] / iters, (double)prof[5] / iters,
-           (long long)iters);
+           (double)prof[2] / iters, (double)prof[8] / iters, (double)prof[9] / iters, (double)prof[10] / iters,
+           (double)prof[3] / iters, (double)prof[4] / iters, (double)prof[5] / iters, (long long)iters);
 #endif
   // ---- write back (F = y G, alpha = y Y) + removeNonsupportPoints ----
   int cnt = 0;
