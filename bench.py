@@ -640,7 +640,7 @@ def run_ours(args):
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
                 "scaling": "strong" if args.strong else "weak",
                 "vs_baseline": None, "dtype": "f32 (fp64 FK and accumulation)", "data": "synthetic",
-                "config": {"workload": "headline", "model": "cfg2 7-DOF arm, M=8", "global_batch": Q_total,
+                "config": {"workload": "headline", "robot": "cfg2 7-DOF arm, M=8", "global_batch": Q_total,
                            "queries_per_gpu": Q, "n_supports": S, "n_cp": M, "dof": wl.robot.dof,
                            "gamma": wl.gamma, "kernel": "gaussian" if wl.kind == 0 else "rq",
                            "parallelism": f"dp{ws} ({'contiguous shards of one batch' if args.strong else 'a batch per rank'}"
