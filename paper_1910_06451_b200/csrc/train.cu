@@ -545,13 +545,35 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
         }
 #pragma unroll
         for (int k = 0; k < EPT; ++k) {
+          // slots past the slice (whole rounds of 256: uniform over the CTA) hold G = +inf and
+          // need no column entry; with the planes in global memory (GPTS: 8 slots per thread
+          // for ~5 live ones at cfg5 scale) they were 3/8 of a computed column's time
+          if (k * kTrainNT >= len) {
+            kr[k] = 0.0f;
+            continue;
+          }
+          // GPTS: all of the slot's plane reads first (L2 round trips: one batch per slot
+          // instead of one per control-point pair), then the terms
           f2 acc;
+          if (GPTS) {
+            f2 ux[LNP], uy[LNP], uz[LNP];
 #pragma unroll
-          for (int p = 0; p < LNP; ++p) {
-            const f2 ux = s_pts[(int64_t)(p * 3 + 0) * A.chunk + koff[k]];
-            const f2 uy = s_pts[(int64_t)(p * 3 + 1) * A.chunk + koff[k]];
-            const f2 uz = s_pts[(int64_t)(p * 3 + 2) * A.chunk + koff[k]];
-            accum_term<LKIND>(acc, sub2(ux, vx[p]), sub2(uy, vy[p]), sub2(uz, vz[p]), p == 0);
+            for (int p = 0; p < LNP; ++p) {
+              ux[p] = s_pts[(int64_t)(p * 3 + 0) * A.chunk + koff[k]];
+              uy[p] = s_pts[(int64_t)(p * 3 + 1) * A.chunk + koff[k]];
+              uz[p] = s_pts[(int64_t)(p * 3 + 2) * A.chunk + koff[k]];
+            }
+#pragma unroll
+            for (int p = 0; p < LNP; ++p)
+              accum_term<LKIND>(acc, sub2(ux[p], vx[p]), sub2(uy[p], vy[p]), sub2(uz[p], vz[p]), p == 0);
+          } else {
+#pragma unroll
+            for (int p = 0; p < LNP; ++p) {
+              const f2 ux = s_pts[(int64_t)(p * 3 + 0) * A.chunk + koff[k]];
+              const f2 uy = s_pts[(int64_t)(p * 3 + 1) * A.chunk + koff[k]];
+              const f2 uz = s_pts[(int64_t)(p * 3 + 2) * A.chunk + koff[k]];
+              accum_term<LKIND>(acc, sub2(ux, vx[p]), sub2(uy, vy[p]), sub2(uz, vz[p]), p == 0);
+            }
           }
           const float ks = pair_sum(acc);
           const float v = A.m_pow2 ? ks * A.inv_m : __fdiv_rn(ks, (float)A.M);
