@@ -103,6 +103,7 @@ struct TrainArgs {
   int64_t cache_cols;
   int32_t M, m_pow2;
   float inv_m;
+  int32_t smem_planes;   // GPTS instances: the first planes of a slice stay in shared memory
 };
 
 __device__ __forceinline__ Cand cand_none(bool for_max) { return Cand{for_max ? 0ull : ~0ull, 0.0, kNone, 1, -1, 0}; }
@@ -299,7 +300,10 @@ __device__ __forceinline__ Decision decide_removal(Decision d, const Cand& b, in
 // ONE: single-CTA instance (launched with C = 1 only) that keeps the winners' payload beside
 // the warp winners (the dependent shared-memory load after the REDUX costs it more than
 // the wider records: N = 1,000 0.80 against 0.81 us per iteration).
-template <int EPT, int LMP, int LKIND, bool GPTS = false, bool ONE = false>
+// NSPL (GPTS only): planes [0, NSPL) of a slice stay in shared memory, the rest in L2 — a
+// compile-time split, so every plane access is a plain LDS or LDG (a runtime split through
+// generic pointers cost more than it saved: 2.70 -> 3.23 us per iteration at cfg5 scale).
+template <int EPT, int LMP, int LKIND, bool GPTS = false, bool ONE = false, int NSPL = 0>
 __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constant__ TrainArgs A) {
   constexpr bool LAZY = LMP > 0;
   constexpr int LNP = LAZY ? LMP / 2 : 1;
@@ -316,10 +320,14 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
   // its own points, so consecutive lanes read consecutive 8-byte words — conflict-free
   // (a per-point record layout put every lane on the same banks: 32-way conflicts, ~11k
   // cycles per computed column). Then the cache slot of each local index's K column.
-  f2* s_pts = GPTS ? A.gpts + (int64_t)rank * LNP * 3 * A.chunk
-                   : reinterpret_cast<f2*>(smem_raw + ((A.chunk * 8 + 15) & ~15ll));
-  int32_t* s_slot = GPTS ? reinterpret_cast<int32_t*>(smem_raw + ((A.chunk * 8 + 15) & ~15ll))
-                         : reinterpret_cast<int32_t*>(s_pts + (LAZY ? A.chunk * LNP * 3 : 0));
+  // GPTS: planes [0, smem_planes) of the slice in shared memory, the rest in the workspace
+  // (L2): at cfg5 scale 20 of the 24 planes fit, so a computed column reads 40 KB instead
+  // of 240 KB through L2.
+  f2* s_pts = reinterpret_cast<f2*>(smem_raw + ((A.chunk * 8 + 15) & ~15ll));
+  f2* g_pts = GPTS ? A.gpts + (int64_t)rank * LNP * 3 * A.chunk : nullptr;
+  constexpr int n_spl = GPTS ? NSPL : LNP * 3;
+  int32_t* s_slot = reinterpret_cast<int32_t*>(s_pts + (LAZY ? A.chunk * n_spl : 0));
+  // (plane pl = p * 3 + coord; pl is a constant after unrolling, so pl < n_spl folds)
   __shared__ __align__(16) WCand s_warp[2][kTrainWarps];
   __shared__ double s_wY[2][ONE ? kTrainWarps : 1];      // ONE: Y and cache slot of the warp winners
   __shared__ int32_t s_wslot[2][ONE ? kTrainWarps : 1];
@@ -355,12 +363,16 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
       s_slot[j] = -1;
       const int64_t g = lo + j;
       const float* src = A.packed + (g / kTileSupports) * LTF + (g % kTileSupports) * LNP * 8;
+#pragma unroll
       for (int p = 0; p < LNP; ++p) {
         const float4 xy = *reinterpret_cast<const float4*>(src + p * 8);
         const float2 zz = *reinterpret_cast<const float2*>(src + p * 8 + 4);
-        s_pts[(int64_t)(p * 3 + 0) * A.chunk + j] = pk(xy.x, xy.y);
-        s_pts[(int64_t)(p * 3 + 1) * A.chunk + j] = pk(xy.z, xy.w);
-        s_pts[(int64_t)(p * 3 + 2) * A.chunk + j] = pk(zz.x, zz.y);
+        if (p * 3 + 0 < n_spl) s_pts[(int64_t)(p * 3 + 0) * A.chunk + j] = pk(xy.x, xy.y);
+        else g_pts[(int64_t)(p * 3 + 0) * A.chunk + j] = pk(xy.x, xy.y);
+        if (p * 3 + 1 < n_spl) s_pts[(int64_t)(p * 3 + 1) * A.chunk + j] = pk(xy.z, xy.w);
+        else g_pts[(int64_t)(p * 3 + 1) * A.chunk + j] = pk(xy.z, xy.w);
+        if (p * 3 + 2 < n_spl) s_pts[(int64_t)(p * 3 + 2) * A.chunk + j] = pk(zz.x, zz.y);
+        else g_pts[(int64_t)(p * 3 + 2) * A.chunk + j] = pk(zz.x, zz.y);
       }
     }
   }
@@ -559,9 +571,12 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
             f2 ux[LNP], uy[LNP], uz[LNP];
 #pragma unroll
             for (int p = 0; p < LNP; ++p) {
-              ux[p] = s_pts[(int64_t)(p * 3 + 0) * A.chunk + koff[k]];
-              uy[p] = s_pts[(int64_t)(p * 3 + 1) * A.chunk + koff[k]];
-              uz[p] = s_pts[(int64_t)(p * 3 + 2) * A.chunk + koff[k]];
+              ux[p] = (p * 3 + 0 < n_spl) ? s_pts[(int64_t)(p * 3 + 0) * A.chunk + koff[k]]
+                                          : g_pts[(int64_t)(p * 3 + 0) * A.chunk + koff[k]];
+              uy[p] = (p * 3 + 1 < n_spl) ? s_pts[(int64_t)(p * 3 + 1) * A.chunk + koff[k]]
+                                          : g_pts[(int64_t)(p * 3 + 1) * A.chunk + koff[k]];
+              uz[p] = (p * 3 + 2 < n_spl) ? s_pts[(int64_t)(p * 3 + 2) * A.chunk + koff[k]]
+                                          : g_pts[(int64_t)(p * 3 + 2) * A.chunk + koff[k]];
             }
 #pragma unroll
             for (int p = 0; p < LNP; ++p)
@@ -809,13 +824,13 @@ static int train_cluster_size(int64_t n, int64_t chunk_max) {
   return (int)C;
 }
 
-template <int EPT, int LMP = 0, int LKIND = 0, bool GPTS = false, bool ONE = false>
+template <int EPT, int LMP = 0, int LKIND = 0, bool GPTS = false, bool ONE = false, int NSPL = 0>
 static cudaError_t launch_ept(const TrainArgs& A, int C, cudaStream_t st, size_t smem) {
   static std::atomic<int> attr[kMaxDevices];
   const int dev = device_slot();
   if (!attr[dev].load()) {
-    cudaFuncSetAttribute(train_kernel<EPT, LMP, LKIND, GPTS, ONE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(train_kernel<EPT, LMP, LKIND, GPTS, ONE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(train_kernel<EPT, LMP, LKIND, GPTS, ONE, NSPL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(train_kernel<EPT, LMP, LKIND, GPTS, ONE, NSPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          220 * 1024);
     attr[dev].store(1);
   }
@@ -831,7 +846,7 @@ static cudaError_t launch_ept(const TrainArgs& A, int C, cudaStream_t st, size_t
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, train_kernel<EPT, LMP, LKIND, GPTS, ONE>, A);
+  return cudaLaunchKernelEx(&cfg, train_kernel<EPT, LMP, LKIND, GPTS, ONE, NSPL>, A);
 }
 
 cudaError_t launch_train(const float* K, int64_t n, int64_t ldk, const int8_t* y, double beta, int64_t iter_max,
@@ -861,6 +876,7 @@ cudaError_t launch_train(const float* K, int64_t n, int64_t ldk, const int8_t* y
   A.M = 1;
   A.m_pow2 = 1;
   A.inv_m = 1.0f;
+  A.smem_planes = 0;
   const int64_t ept = (A.chunk + kTrainNT - 1) / kTrainNT;
   const size_t smem = (size_t)A.chunk * 8;
   cudaError_t e;
@@ -882,6 +898,7 @@ cudaError_t launch_train(const float* K, int64_t n, int64_t ldk, const int8_t* y
 // ---- lazy-column mode ----
 constexpr int64_t kLazySmem = 200 * 1024;  // shared-memory budget per CTA
 constexpr int kLazyMaxEPT = 8;             // slots per thread in the lazy mode
+constexpr int64_t kLazySmemGpts = 217 * 1024;  // GPTS instances: shared memory for Y, slots and the first planes
 
 static int64_t lazy_bytes_per_slot(int MP) { return 8 + 4 + (int64_t)(MP / 2) * 24; }
 
@@ -912,9 +929,15 @@ size_t train_lazy_plane_bytes(int64_t n, int M) {
   return (size_t)C * chunk * (MP / 2) * 3 * sizeof(f2);
 }
 
+// planes a GPTS instance can keep in shared memory: 5/6 of the slice's (20 of 24 at M = 16:
+// 1,250 points x 160 B + Y + slots = 215 KB), or none when the slice is too long for that
+constexpr int gpts_split_planes(int mp) { return (mp / 2) * 3 * 5 / 6; }
+
 template <int MP, int KIND>
 static cudaError_t launch_lazy_mp(const TrainArgs& A, int C, cudaStream_t st, size_t smem) {
   const int64_t ept = (A.chunk + kTrainNT - 1) / kTrainNT;
+  if (A.gpts && A.smem_planes > 0)
+    return launch_ept<kLazyMaxEPT, MP, KIND, true, false, gpts_split_planes(MP)>(A, C, st, smem);
   if (A.gpts) return launch_ept<kLazyMaxEPT, MP, KIND, true>(A, C, st, smem);
   if (ept <= 2) return launch_ept<2, MP, KIND>(A, C, st, smem);
   if (ept <= 4) return launch_ept<4, MP, KIND>(A, C, st, smem);
@@ -947,12 +970,20 @@ cudaError_t launch_train_lazy(const float* packed, int64_t n, int M, int kind, c
   if (A.chunk < 1) A.chunk = 1;
   A.packed = packed;
   A.gpts = gpts ? static_cast<f2*>(planes) : nullptr;
+  A.smem_planes = 0;
+  if (gpts) {  // the split instance when its planes fit, else every plane in L2
+    const int64_t fixed = ((A.chunk * 8 + 15) & ~15ll) + A.chunk * 4;
+    const int sp = gpts_split_planes(MP);
+    const char* e = getenv("FASTRON_LAZY_SMEM_PLANES");  // "0": the all-L2 instance (tests, A/B)
+    if (sp > 0 && fixed + A.chunk * 8 * sp <= kLazySmemGpts && !(e && e[0] == '0')) A.smem_planes = sp;
+  }
   A.cache = cache;
   A.cache_cols = cache_cols;
   A.M = M;
   A.m_pow2 = (M & (M - 1)) == 0;
   A.inv_m = 1.0f / (float)M;
-  const size_t smem = (size_t)((A.chunk * 8 + 15) & ~15ll) + (gpts ? 0 : (size_t)A.chunk * (MP / 2) * 24) +
+  const size_t smem = (size_t)((A.chunk * 8 + 15) & ~15ll) +
+                      (gpts ? (size_t)A.chunk * 8 * A.smem_planes : (size_t)A.chunk * (MP / 2) * 24) +
                       (size_t)A.chunk * 4;
   cudaError_t e;
   switch (MP) {

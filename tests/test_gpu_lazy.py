@@ -142,10 +142,15 @@ def test_lazy_global_planes_forced(tmp_path):
     yd = dev(y)
     for kind, cache in ((0, 4096), (1, 13)):
         ref = fb.fastron_train_lazy(pos, yd, kind, wl.gamma, 1.0, 3000, cache_cols=cache)
-        os.environ["FASTRON_LAZY_GPTS"] = "1"
-        try:
-            got = fb.fastron_train_lazy(pos, yd, kind, wl.gamma, 1.0, 3000, cache_cols=cache)
-        finally:
-            os.environ.pop("FASTRON_LAZY_GPTS", None)
-        torch.cuda.synchronize()
-        _same(ref, got)
+        # the all-L2 instance and the split one (5/6 of the slice's planes in shared memory)
+        for planes in ("0", None):
+            os.environ["FASTRON_LAZY_GPTS"] = "1"
+            if planes is not None:
+                os.environ["FASTRON_LAZY_SMEM_PLANES"] = planes
+            try:
+                got = fb.fastron_train_lazy(pos, yd, kind, wl.gamma, 1.0, 3000, cache_cols=cache)
+            finally:
+                os.environ.pop("FASTRON_LAZY_GPTS", None)
+                os.environ.pop("FASTRON_LAZY_SMEM_PLANES", None)
+            torch.cuda.synchronize()
+            _same(ref, got)
