@@ -886,6 +886,7 @@ cudaError_t launch_train(const float* K, int64_t n, int64_t ldk, const int8_t* y
   if (C == 1 && ept <= E) e = launch_ept<E, 0, 0, false, true>(A, C, st, smem);
   else if (C == 1 && ept <= 2 * E) e = launch_ept<2 * E, 0, 0, false, true>(A, C, st, smem);
   else if (ept <= E) e = launch_ept<E>(A, C, st, smem);
+  else if (ept <= E + E / 2) e = launch_ept<E + E / 2>(A, C, st, smem);  // 6 slots: N = 20,000 on 16 CTAs (5 live)
   else if (ept <= 2 * E) e = launch_ept<2 * E>(A, C, st, smem);
   else if (ept <= 3 * E) e = launch_ept<3 * E>(A, C, st, smem);
   else if (ept <= 4 * E) e = launch_ept<4 * E>(A, C, st, smem);
@@ -936,8 +937,10 @@ constexpr int gpts_split_planes(int mp) { return (mp / 2) * 3 * 5 / 6; }
 template <int MP, int KIND>
 static cudaError_t launch_lazy_mp(const TrainArgs& A, int C, cudaStream_t st, size_t smem) {
   const int64_t ept = (A.chunk + kTrainNT - 1) / kTrainNT;
-  if (A.gpts && A.smem_planes > 0)
+  if (A.gpts && A.smem_planes > 0) {  // 6 slots where they cover the slice (cfg5 scale: 5 live)
+    if (ept <= 6) return launch_ept<6, MP, KIND, true, false, gpts_split_planes(MP)>(A, C, st, smem);
     return launch_ept<kLazyMaxEPT, MP, KIND, true, false, gpts_split_planes(MP)>(A, C, st, smem);
+  }
   if (A.gpts) return launch_ept<kLazyMaxEPT, MP, KIND, true>(A, C, st, smem);
   if (ept <= 2) return launch_ept<2, MP, KIND>(A, C, st, smem);
   if (ept <= 4) return launch_ept<4, MP, KIND>(A, C, st, smem);
