@@ -555,6 +555,19 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
           vy[LNP - 1] &= 0xffffffffull;
           vz[LNP - 1] &= 0xffffffffull;
         }
+        // split GPTS instance: the few planes that live in L2, for every live slot, in one
+        // batch up front (the cache stores between the slots would otherwise fence each
+        // slot's loads behind the previous slot's store: one L2 round trip per slot)
+        constexpr int NG = (GPTS && NSPL > 0) ? LNP * 3 - NSPL : 0;
+        f2 gq[NG > 0 ? EPT : 1][NG > 0 ? NG : 1];
+        if (NG > 0) {
+#pragma unroll
+          for (int k = 0; k < EPT; ++k) {
+            if (k * kTrainNT >= len) continue;
+#pragma unroll
+            for (int g = 0; g < NG; ++g) gq[k][g] = g_pts[(int64_t)(NSPL + g) * A.chunk + koff[k]];
+          }
+        }
 #pragma unroll
         for (int k = 0; k < EPT; ++k) {
           // slots past the slice (whole rounds of 256: uniform over the CTA) hold G = +inf and
@@ -571,12 +584,13 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
             f2 ux[LNP], uy[LNP], uz[LNP];
 #pragma unroll
             for (int p = 0; p < LNP; ++p) {
-              ux[p] = (p * 3 + 0 < n_spl) ? s_pts[(int64_t)(p * 3 + 0) * A.chunk + koff[k]]
-                                          : g_pts[(int64_t)(p * 3 + 0) * A.chunk + koff[k]];
-              uy[p] = (p * 3 + 1 < n_spl) ? s_pts[(int64_t)(p * 3 + 1) * A.chunk + koff[k]]
-                                          : g_pts[(int64_t)(p * 3 + 1) * A.chunk + koff[k]];
-              uz[p] = (p * 3 + 2 < n_spl) ? s_pts[(int64_t)(p * 3 + 2) * A.chunk + koff[k]]
-                                          : g_pts[(int64_t)(p * 3 + 2) * A.chunk + koff[k]];
+#define FASTRON_PL(pl)                                                                      \
+  ((pl) < n_spl ? s_pts[(int64_t)(pl) * A.chunk + koff[k]]                                  \
+                : NG > 0 ? gq[k][(pl) - n_spl < 0 ? 0 : (pl) - n_spl] : g_pts[(int64_t)(pl) * A.chunk + koff[k]])
+              ux[p] = FASTRON_PL(p * 3 + 0);
+              uy[p] = FASTRON_PL(p * 3 + 1);
+              uz[p] = FASTRON_PL(p * 3 + 2);
+#undef FASTRON_PL
             }
 #pragma unroll
             for (int p = 0; p < LNP; ++p)
