@@ -117,17 +117,64 @@ __global__ void label_capsules_kernel(const __grid_constant__ CapsuleScene sc, c
   label[k] = hit ? 1 : -1;
 }
 
-// F_j = sum_i alpha_i K[i][j] over the nonzero alpha_i, in index order (deterministic).
-__global__ void matvec_kernel(const float* __restrict__ K, int64_t n, int64_t ldk, const double* __restrict__ alpha,
-                              double* __restrict__ F) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
+// F_j = sum_i alpha_i K[i][j] over the nonzero alpha_i, in index order (deterministic:
+// separately rounded multiply and add, the oracle's order). A warm start's alpha is sparse
+// (the previous support set), and a plain loop over i is one dependent DRAM round trip per
+// nonzero row (8,446 points, 2,482 nonzero: 0.95 ms). Here the CTA first compacts the next
+// nonzero indices, in order, into shared memory (ballot + prefix per 128-index chunk), then
+// every thread walks that list with kMvUnroll row loads in flight and adds them in list
+// order — the same operations in the same order, so the same bits.
+constexpr int kMvNT = 128;
+constexpr int kMvSeg = 2048;    // nonzero entries per shared-memory segment
+constexpr int kMvUnroll = 16;   // K loads in flight per thread
+__global__ void __launch_bounds__(kMvNT) matvec_kernel(const float* __restrict__ K, int64_t n, int64_t ldk,
+                                                       const double* __restrict__ alpha, double* __restrict__ F) {
+  __shared__ int32_t s_idx[kMvSeg];
+  __shared__ double s_a[kMvSeg];
+  __shared__ int s_wcnt[kMvNT / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t j = (int64_t)blockIdx.x * kMvNT + tid;
+  const bool live = j < n;
+  const float* Kj = K + (live ? j : 0);
   double f = 0.0;
-  for (int64_t i = 0; i < n; ++i) {
-    const double a = alpha[i];  // warp-uniform
-    if (a != 0.0) f = __dadd_rn(f, __dmul_rn(a, (double)K[i * ldk + j]));
+  int64_t base = 0;  // next index of alpha to scan (uniform)
+  while (base < n) {
+    int cnt = 0;  // entries in the segment (uniform)
+    while (base < n && cnt + kMvNT <= kMvSeg) {
+      const int64_t i = base + tid;
+      const double a = i < n ? alpha[i] : 0.0;
+      const bool nz = a != 0.0;
+      const unsigned bal = __ballot_sync(0xffffffffu, nz);
+      if (lane == 0) s_wcnt[warp] = __popc(bal);
+      __syncthreads();
+      int ofs = cnt, total = 0;
+#pragma unroll
+      for (int w = 0; w < kMvNT / 32; ++w) {
+        if (w < warp) ofs += s_wcnt[w];
+        total += s_wcnt[w];
+      }
+      if (nz) {
+        const int at = ofs + __popc(bal & ((1u << lane) - 1u));
+        s_idx[at] = (int32_t)i;
+        s_a[at] = a;
+      }
+      cnt += total;
+      base += kMvNT;
+      __syncthreads();
+    }
+    if (live) {
+      for (int t = 0; t < cnt; t += kMvUnroll) {
+        float kv[kMvUnroll];
+#pragma unroll
+        for (int k = 0; k < kMvUnroll; ++k) kv[k] = t + k < cnt ? __ldg(Kj + (int64_t)s_idx[t + k] * ldk) : 0.0f;
+#pragma unroll
+        for (int k = 0; k < kMvUnroll; ++k)
+          if (t + k < cnt) f = __dadd_rn(f, __dmul_rn(s_a[t + k], (double)kv[k]));
+      }
+    }
+    __syncthreads();  // the segment is consumed before it is refilled
   }
-  F[j] = f;
+  if (live) F[j] = f;
 }
 
 template <int MP, int KIND>
@@ -241,7 +288,7 @@ cudaError_t launch_label_capsules(const float4* pos, int64_t ldp, int64_t n, con
 
 cudaError_t launch_matvec(const float* K, int64_t n, int64_t ldk, const double* alpha, double* F, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  matvec_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(K, n, ldk, alpha, F);
+  matvec_kernel<<<(unsigned)((n + kMvNT - 1) / kMvNT), kMvNT, 0, st>>>(K, n, ldk, alpha, F);
   g_launches.fetch_add(1);
   return cudaGetLastError();
 }
