@@ -143,3 +143,28 @@ def test_lazy_update_equals_full_update():
     for k in ("iterations", "n_add", "n_remove", "n_support", "converged"):
         assert rf[k] == rl[k], (k, rf, rl)
     assert torch.equal(full.alpha, lazy.alpha) and torch.equal(full.supports, lazy.supports)
+
+
+@pytest.mark.parametrize("n,nnz", [(1, 1), (130, 0), (777, 777), (3001, 2500), (4500, 4100)])
+def test_matvec_index_order_bit_exact(n, nnz):
+    """fastron_kernel_matvec: F_j = sum over the nonzero alpha_i, in index order, of
+    fl(alpha_i K_ij) with separately rounded fp64 multiply and add (the margins
+    of a loaded model) — bit-exact against that sum written out, on sizes that leave a ragged
+    last CTA, fill several shared-memory segments of nonzero indices (2,048 each) and on an
+    all-zero alpha; K with padded rows (ldk > n)."""
+    require_gpu()
+    import torch
+    import paper_1910_06451_b200 as fb
+    rng = np.random.default_rng(n + nnz)
+    ldk = (n + 7) // 8 * 8 + 8
+    Kh = rng.uniform(0.0, 1.0, (n, ldk)).astype(np.float32)
+    alpha = np.zeros(n)
+    nz = np.sort(rng.choice(n, nnz, replace=False))
+    alpha[nz] = rng.standard_normal(nnz) * 50.0
+    K = dev(Kh)[:, :n]
+    F = fb.fastron_kernel_matvec(K, dev(alpha))
+    torch.cuda.synchronize()
+    ref = np.zeros(n)
+    for i in nz:  # index order; numpy's elementwise fp64 multiply and add round separately
+        ref = ref + alpha[i] * Kh[i, :n].astype(np.float64)
+    assert np.array_equal(F.cpu().numpy(), ref)
