@@ -474,6 +474,10 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
       }
     }
     Cand b = for_max ? best_of8<true>(e) : best_of8<false>(e);
+#ifdef FASTRON_TRAIN_PROF
+    if (b.idx == -12345) prof[11] += 1;  // the tree's result is needed here
+    PROF_MARK(11);
+#endif
     if (b.idx != kNone) {
       b.Y = s_Y[b.idx - lo];
       if (LAZY) b.slot = s_slot[b.idx - lo];
@@ -749,9 +753,10 @@ __global__ void __launch_bounds__(kTrainNT, 1) train_kernel(const __grid_constan
 #ifdef FASTRON_TRAIN_PROF
   if (tid == 0 && rank == 0 && n_miss) printf("train prof computed columns %llu, %.0f cycles each\n", n_miss, (double)prof_miss / n_miss);
   if (tid == 0 && rank == 0)
-    printf("train prof cycles/iter: scan %.0f merge+key %.0f argbest %.0f payload %.0f bar %.0f | cta-best+send %.0f inbox-wait %.0f inbox-best %.0f decide %.0f - %.0f tail %.0f (iters %lld)\n",
+    printf("train prof cycles/iter: scan %.0f merge+key %.0f argbest %.0f payload %.0f bar %.0f | cta-tree %.0f payload+send %.0f inbox-wait %.0f inbox-best %.0f decide %.0f - %.0f tail %.0f (iters %lld)\n",
            (double)prof[0] / iters, (double)prof[6] / iters, (double)prof[7] / iters, (double)prof[1] / iters,
-           (double)prof[2] / iters, (double)prof[8] / iters, (double)prof[9] / iters, (double)prof[10] / iters,
+           (double)prof[2] / iters, (double)prof[11] / iters, (double)prof[8] / iters, (double)prof[9] / iters,
+           (double)prof[10] / iters,
            (double)prof[3] / iters, (double)prof[4] / iters, (double)prof[5] / iters, (long long)iters);
 #endif
   // ---- write back (F = y G, alpha = y Y) + removeNonsupportPoints ----
