@@ -73,6 +73,15 @@ def load_library(path: str = LIB_PATH):
     global _lib
     if _lib is not None:
         return _lib
+    if not os.path.exists(path) and path == LIB_PATH:
+        # a checkout without the built artefact (the .so is git-ignored): build it in-tree
+        # with nvcc once; anything short of the real library is an error (no CPU fallback)
+        try:
+            from . import _build
+            _build.build()
+        except Exception as e:  # nvcc missing, compile error
+            raise ImportError(f"{path} is missing and could not be built ({e}); build it with "
+                              "`python -m paper_1910_06451_b200._build` (there is no CPU fallback)") from e
     if not os.path.exists(path):
         raise ImportError(f"{path} is missing: build it with `python -m paper_1910_06451_b200._build` "
                           "(there is no CPU fallback)")
